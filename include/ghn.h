@@ -1,0 +1,143 @@
+/*
+ * ghn.h -- C ABI of the B200-native Grid Hashing Neighborhood (GHN) path.
+ *
+ * The reference (gridneighbors, pure Python/numpy) has no FFI: its boundary
+ * is the Python API re-exported at pkg/src/gridneighbors/__init__.py:7-36.
+ * This library is the native layer under the drop-in Python mirror
+ * (paper_2004_02290_b200/), loaded with ctypes.  Each entry point names the
+ * reference interface it replaces.
+ *
+ * Conventions
+ *   - every array argument is a DEVICE pointer to caller-owned memory
+ *     (PyTorch tensors in the Python layer) unless documented "host";
+ *   - `stream` is a cudaStream_t (NULL = legacy default stream);
+ *   - return value: GHN_OK or an error code; ghn_last_error() gives a
+ *     thread-local message.  GHN_ERR_VALUE maps to the reference's
+ *     ValueError, the others to RuntimeError;
+ *   - no global mutable state: calls on different streams are independent.
+ */
+#ifndef GHN_H_
+#define GHN_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GHN_MAX_DIM 16
+
+enum { GHN_F32 = 0, GHN_F64 = 1 };
+enum { GHN_LAYOUT_DENSE = 0, GHN_LAYOUT_LIST = 1 };
+enum { GHN_MODE_HEURISTIC = 0, GHN_MODE_GUARANTEED = 1 };           /* explore.py:21 */
+enum { GHN_TASK_NONE = 0, GHN_TASK_CLASSIFY = 1, GHN_TASK_REGRESS_MEAN = 2 };
+enum { GHN_OK = 0, GHN_ERR_VALUE = 1, GHN_ERR_CUDA = 2, GHN_ERR_UNSUPPORTED = 3 };
+
+/* Thread-local description of the last failure on this thread. */
+const char *ghn_last_error(void);
+/* ABI version (major*100 + minor). */
+int32_t ghn_abi_version(void);
+
+/* ------------------------------------------------------------------ fit
+ * Replaces grid.build (grid.py:165-195) together with _hash_all
+ * (grid.py:124-125) and the finite check of LabeledPoint (core.py:35-36).
+ *
+ * Phase 1 -- ghn_fit_bounds: per-dimension cell-id bounds lo/hi of
+ * floor(x / w) (IEEE fp64), origin = per-dimension minimum coordinate
+ * (GridParams.origin, grid.py:109), and a non-finite flag.
+ *   X          (n, d) row-major, dtype GHN_F32 or GHN_F64
+ *   widths     host, d doubles > 0
+ *   out_bounds int64[2*d]: lo[0..d), hi[0..d)
+ *   out_origin double[d]
+ *   out_flags  int32[1]: bit0 = a non-finite coordinate was seen
+ */
+int32_t ghn_fit_bounds(const void *X, int32_t dtype, int64_t n, int32_t d, const double *widths,
+                       int64_t *out_bounds, double *out_origin, int32_t *out_flags, void *stream);
+
+/* Host-only plan: chooses the cell-table layout from the bounds and sizes
+ * the workspace.  DENSE = offsets over the whole id bounding box (E cells);
+ * LIST = sorted non-empty cell list only (for huge, sparse boxes). */
+typedef struct ghn_fit_plan {
+    int64_t n;
+    int32_t d;
+    int32_t dtype;
+    int32_t layout;
+    int32_t key_bits;                 /* bits of the dense linear key (DENSE) */
+    int64_t E;                        /* cells in the id bounding box (DENSE) */
+    double widths[GHN_MAX_DIM];
+    int64_t lo[GHN_MAX_DIM];
+    int64_t ext[GHN_MAX_DIM];         /* hi - lo + 1 */
+    size_t workspace_bytes;
+} ghn_fit_plan;
+
+int32_t ghn_fit_plan_init(ghn_fit_plan *plan, int64_t n, int32_t d, int32_t dtype,
+                          const double *widths, const int64_t *bounds_host, int64_t dense_limit);
+
+/* Outputs of phase 2.  Capacities: perm n; coords d*n; cell_start n+1;
+ * cell_ids n*d; pt_off / ne_off E+1 (DENSE only, else NULL). */
+typedef struct ghn_fit_out {
+    int32_t *perm;        /* CSR slot -> original point index (= concat(buckets)) */
+    void *coords;         /* permuted coordinates, SoA: coords[j*n + slot], dtype */
+    int32_t *cell_start;  /* non-empty cell c holds slots [cell_start[c], cell_start[c+1]) */
+    int32_t *cell_ids;    /* (C_ne, d) ids relative to lo, lexicographic (= cell_array - lo) */
+    int32_t *n_cells;     /* scalar C_ne */
+    int32_t *pt_off;      /* DENSE: slots before linear cell key c (E+1) */
+    int32_t *ne_off;      /* DENSE: non-empty cells before linear cell key c (E+1) */
+} ghn_fit_out;
+
+/* Phase 2: stable LSD radix sort by cell (ties keep input order, as the
+ * lexsort of grid.py:188-189), CSR extraction, dense tables, SoA gather. */
+int32_t ghn_fit_build(const ghn_fit_plan *plan, const void *X, const ghn_fit_out *out,
+                      void *workspace, size_t workspace_bytes, void *stream);
+
+/* ---------------------------------------------------------------- query
+ * Replaces explore.knn_query (explore.py:66-137) with core.ordering_keys /
+ * keys_to_distances (core.py:72-91), batched over nq queries, with the
+ * predict.classify / predict.regress(agg="mean") epilogue (predict.py:20-47)
+ * fused. */
+typedef struct ghn_index_view {
+    int64_t n;
+    int32_t d;
+    int32_t dtype;
+    int32_t layout;
+    int32_t n_cells;
+    int64_t E;
+    double widths[GHN_MAX_DIM];
+    double min_width;
+    int64_t lo[GHN_MAX_DIM];
+    int64_t ext[GHN_MAX_DIM];
+    const void *coords;          /* SoA permuted, dtype */
+    const int32_t *perm;
+    const int32_t *cell_start;
+    const int32_t *cell_ids;
+    const int32_t *pt_off;       /* DENSE */
+    const int32_t *ne_off;       /* DENSE */
+    const int32_t *labels;       /* original point order; classify only */
+    const double *targets;       /* original point order; regress only */
+} ghn_index_view;
+
+typedef struct ghn_query_out {
+    double *dist;                /* (nq, k) sqrt(key) fp64, or NULL */
+    int64_t *idx;                /* (nq, k) original point index, or NULL */
+    int32_t *label;              /* (nq) CLASSIFY: winning label code, or NULL */
+    double *confidence;          /* (nq) CLASSIFY: count / k, or NULL */
+    double *value;               /* (nq) REGRESS_MEAN: mean target, or NULL */
+    int64_t *stats;              /* (nq, 3) layers_visited, cells_visited, points_scanned, or NULL */
+    unsigned long long *totals;  /* [4] += sum layers, cells, points, queries, or NULL */
+} ghn_query_out;
+
+/* Workspace for query binning (sorting queries by their central cell). */
+size_t ghn_query_workspace_size(const ghn_index_view *ix, int64_t nq);
+
+/* Q is (nq, d) row-major, dtype q_dtype (GHN_F32 / GHN_F64, independent of
+ * the index dtype: queries are upcast to fp64 like explore.py:83).
+ * 1 <= k <= n and k <= 256. */
+int32_t ghn_query(const ghn_index_view *ix, const void *Q, int32_t q_dtype, int64_t nq, int32_t k, int32_t mode,
+                  int32_t task, const ghn_query_out *out, void *workspace, size_t workspace_bytes,
+                  void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GHN_H_ */

@@ -1,0 +1,135 @@
+"""ctypes binding of libghn.so (include/ghn.h).
+
+The product path has no CPU fallback: if the library or a CUDA device is
+missing, every device entry point raises RuntimeError.  Struct layouts here
+mirror include/ghn.h field for field.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libghn.so")
+
+GHN_MAX_DIM = 16
+GHN_F32, GHN_F64 = 0, 1
+GHN_LAYOUT_DENSE, GHN_LAYOUT_LIST = 0, 1
+GHN_MODE = {"heuristic": 0, "guaranteed": 1}
+GHN_TASK_NONE, GHN_TASK_CLASSIFY, GHN_TASK_REGRESS_MEAN = 0, 1, 2
+GHN_OK, GHN_ERR_VALUE, GHN_ERR_CUDA, GHN_ERR_UNSUPPORTED = 0, 1, 2, 3
+
+# Every symbol include/ghn.h declares (checked by tests/test_abi.py).
+EXPORTS = (
+    "ghn_last_error",
+    "ghn_abi_version",
+    "ghn_fit_bounds",
+    "ghn_fit_plan_init",
+    "ghn_fit_build",
+    "ghn_query_workspace_size",
+    "ghn_query",
+)
+
+_i64, _i32, _f64, _p, _sz = ctypes.c_int64, ctypes.c_int32, ctypes.c_double, ctypes.c_void_p, ctypes.c_size_t
+
+
+class FitPlan(ctypes.Structure):
+    _fields_ = [
+        ("n", _i64), ("d", _i32), ("dtype", _i32), ("layout", _i32), ("key_bits", _i32),
+        ("E", _i64),
+        ("widths", _f64 * GHN_MAX_DIM),
+        ("lo", _i64 * GHN_MAX_DIM),
+        ("ext", _i64 * GHN_MAX_DIM),
+        ("workspace_bytes", _sz),
+    ]
+
+
+class FitOut(ctypes.Structure):
+    _fields_ = [
+        ("perm", _p), ("coords", _p), ("cell_start", _p), ("cell_ids", _p), ("n_cells", _p),
+        ("pt_off", _p), ("ne_off", _p),
+    ]
+
+
+class IndexView(ctypes.Structure):
+    _fields_ = [
+        ("n", _i64), ("d", _i32), ("dtype", _i32), ("layout", _i32), ("n_cells", _i32),
+        ("E", _i64),
+        ("widths", _f64 * GHN_MAX_DIM),
+        ("min_width", _f64),
+        ("lo", _i64 * GHN_MAX_DIM),
+        ("ext", _i64 * GHN_MAX_DIM),
+        ("coords", _p), ("perm", _p), ("cell_start", _p), ("cell_ids", _p),
+        ("pt_off", _p), ("ne_off", _p), ("labels", _p), ("targets", _p),
+    ]
+
+
+class QueryOut(ctypes.Structure):
+    _fields_ = [
+        ("dist", _p), ("idx", _p), ("label", _p), ("confidence", _p), ("value", _p),
+        ("stats", _p), ("totals", _p),
+    ]
+
+
+_lib = None
+
+
+def available() -> bool:
+    return os.path.exists(LIB_PATH)
+
+
+def lib():
+    """Load libghn.so; raise RuntimeError (never fall back) if it cannot be used."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise RuntimeError(
+            f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'`")
+    L = ctypes.CDLL(LIB_PATH)
+    L.ghn_last_error.restype = ctypes.c_char_p
+    L.ghn_abi_version.restype = _i32
+    L.ghn_fit_bounds.argtypes = [_p, _i32, _i64, _i32, _p, _p, _p, _p, _p]
+    L.ghn_fit_bounds.restype = _i32
+    L.ghn_fit_plan_init.argtypes = [ctypes.POINTER(FitPlan), _i64, _i32, _i32, _p, _p, _i64]
+    L.ghn_fit_plan_init.restype = _i32
+    L.ghn_fit_build.argtypes = [ctypes.POINTER(FitPlan), _p, ctypes.POINTER(FitOut), _p, _sz, _p]
+    L.ghn_fit_build.restype = _i32
+    L.ghn_query_workspace_size.argtypes = [ctypes.POINTER(IndexView), _i64]
+    L.ghn_query_workspace_size.restype = _sz
+    L.ghn_query.argtypes = [ctypes.POINTER(IndexView), _p, _i32, _i64, _i32, _i32, _i32,
+                            ctypes.POINTER(QueryOut), _p, _sz, _p]
+    L.ghn_query.restype = _i32
+    _lib = L
+    return L
+
+
+def check(rc: int, what: str) -> None:
+    """Map a ghn status to the reference's exception convention."""
+    if rc == GHN_OK:
+        return
+    msg = lib().ghn_last_error().decode(errors="replace")
+    if rc == GHN_ERR_VALUE:
+        raise ValueError(f"{what}: {msg}")
+    raise RuntimeError(f"{what} failed (rc={rc}): {msg}")
+
+
+def require_device():
+    """The CUDA path or nothing: raise if no GPU or no library."""
+    import torch
+
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_2004_02290_b200 requires a CUDA device (B200); no CPU fallback")
+    return lib()
+
+
+def ptr(t) -> int:
+    return 0 if t is None else int(t.data_ptr())
+
+
+def stream_handle(stream=None) -> int:
+    import torch
+
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return int(s.cuda_stream)

@@ -1,0 +1,172 @@
+// ghn_common.cuh -- shared device helpers for the GHN sm_100a kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "ghn.h"
+
+#define GHN_FULL 0xffffffffu
+
+namespace ghn {
+
+// ---------------------------------------------------------------- errors
+void set_error(const char *fmt, ...);
+int32_t cuda_status(cudaError_t e, const char *where);
+
+#define GHN_CUDA_CHECK(expr)                                           \
+    do {                                                               \
+        cudaError_t _e = (expr);                                       \
+        if (_e != cudaSuccess) return ::ghn::cuda_status(_e, #expr);   \
+    } while (0)
+
+#define GHN_LAUNCH_CHECK(where)                                        \
+    do {                                                               \
+        cudaError_t _e = cudaGetLastError();                           \
+        if (_e != cudaSuccess) return ::ghn::cuda_status(_e, where);   \
+    } while (0)
+
+// ---------------------------------------------------------------- numerics
+// Cell id: floor(x / w) in IEEE fp64 (grid.py:125, explore.py:91).  When w is
+// a power of two, x * (1/w) is the same exactly-representable real value and
+// rounds identically, so the reciprocal multiply is bit-exact.
+__device__ __forceinline__ int64_t cell_id(double x, double w, double inv_w, bool pow2) {
+    double t = pow2 ? __dmul_rn(x, inv_w) : __ddiv_rn(x, w);
+    double f = floor(t);
+    // clamp far outliers (|id| >= 2^62) so integer arithmetic cannot overflow
+    f = fmin(fmax(f, -4.6116860184273879e18), 4.6116860184273879e18);
+    return (int64_t)f;
+}
+
+// Squared L2 key in numpy's einsum('ij,ij->i') order (core.py:80):
+// two SSE2 lanes (even / odd coordinates); each 8-wide chunk is folded as a
+// reversed chain of 4 pairs; remaining pairs forward; lane0 + lane1; no FMA.
+template <int D>
+__device__ __forceinline__ double key_numpy_order(const double (&diff)[D]) {
+    double a0 = 0.0, a1 = 0.0;
+    int j = 0;
+#pragma unroll
+    for (int c = 0; c < D / 8; ++c, j += 8) {
+#pragma unroll
+        for (int p = 3; p >= 0; --p) {
+            a0 = __dadd_rn(__dmul_rn(diff[j + 2 * p], diff[j + 2 * p]), a0);
+            a1 = __dadd_rn(__dmul_rn(diff[j + 2 * p + 1], diff[j + 2 * p + 1]), a1);
+        }
+    }
+#pragma unroll
+    for (; j < D; j += 2) {
+        a0 = __dadd_rn(__dmul_rn(diff[j], diff[j]), a0);
+        if (j + 1 < D) a1 = __dadd_rn(__dmul_rn(diff[j + 1], diff[j + 1]), a1);
+    }
+    return __dadd_rn(a0, a1);
+}
+
+// Runtime-d variant (d <= GHN_MAX_DIM), same order.
+__device__ __forceinline__ double key_numpy_order_rt(const double *diff, int d) {
+    double a0 = 0.0, a1 = 0.0;
+    int j = 0;
+    for (; d - j >= 8; j += 8) {
+        for (int p = 3; p >= 0; --p) {
+            a0 = __dadd_rn(__dmul_rn(diff[j + 2 * p], diff[j + 2 * p]), a0);
+            a1 = __dadd_rn(__dmul_rn(diff[j + 2 * p + 1], diff[j + 2 * p + 1]), a1);
+        }
+    }
+    for (; j < d; j += 2) {
+        a0 = __dadd_rn(__dmul_rn(diff[j], diff[j]), a0);
+        if (j + 1 < d) a1 = __dadd_rn(__dmul_rn(diff[j + 1], diff[j + 1]), a1);
+    }
+    return __dadd_rn(a0, a1);
+}
+
+// (key, index) lexicographic order (explore.py:114).
+__device__ __forceinline__ bool pair_less(double ka, int32_t ia, double kb, int32_t ib) {
+    return ka < kb || (ka == kb && ia < ib);
+}
+
+__device__ __forceinline__ double shfl_d(double v, int src) {
+    return __shfl_sync(GHN_FULL, v, src);
+}
+
+__device__ __forceinline__ unsigned lanemask_lt() {
+    unsigned m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+__device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
+
+template <typename T>
+__device__ __forceinline__ T warp_inclusive_scan(T v) {
+    const int lane = lane_id();
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        T u = __shfl_up_sync(GHN_FULL, v, o);
+        if (lane >= o) v += u;
+    }
+    return v;
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(GHN_FULL, v, o);
+    return v;
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_min(T v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        T u = __shfl_xor_sync(GHN_FULL, v, o);
+        v = u < v ? u : v;
+    }
+    return v;
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_max(T v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        T u = __shfl_xor_sync(GHN_FULL, v, o);
+        v = u > v ? u : v;
+    }
+    return v;
+}
+
+__device__ __forceinline__ double to_double(float x) { return (double)x; }
+__device__ __forceinline__ double to_double(double x) { return x; }
+
+// Order-preserving encoding of doubles into uint64 (for atomicMin).
+__device__ __forceinline__ unsigned long long dbl_order_key(double v) {
+    unsigned long long b = (unsigned long long)__double_as_longlong(v);
+    return (b & 0x8000000000000000ull) ? ~b : (b | 0x8000000000000000ull);
+}
+__host__ __device__ inline double dbl_from_order_key(unsigned long long k) {
+    unsigned long long b = (k & 0x8000000000000000ull) ? (k & 0x7fffffffffffffffull) : ~k;
+    double v;
+    memcpy(&v, &b, sizeof(v));
+    return v;
+}
+
+inline bool is_pow2_width(double w, double *inv) {
+    int e;
+    double m = frexp(w, &e);
+    if (m != 0.5) return false;
+    *inv = ldexp(1.0, 1 - e);
+    return (*inv) * w == 1.0 && isfinite(*inv) && *inv != 0.0;
+}
+
+// ---------------------------------------------------------------- scan / sort
+// Device-wide exclusive scan of int32 (in may alias out).  Workspace bytes:
+size_t scan_workspace_bytes(int64_t len);
+int32_t exclusive_scan_i32(const int32_t *in, int32_t *out, int64_t len, void *ws, cudaStream_t s);
+
+// Stable LSD radix sort of (uint32 key, int32 value) pairs over key bits
+// [0, bits).  vals_in == NULL means "values are 0..n-1".  Results land in
+// (keys_out, vals_out); the *_tmp buffers are ping-pong scratch.
+size_t radix_workspace_bytes(int64_t n);
+int32_t radix_sort_pairs(const uint32_t *keys_in, const int32_t *vals_in, uint32_t *keys_out,
+                         int32_t *vals_out, uint32_t *keys_tmp, int32_t *vals_tmp, int64_t n,
+                         int bits, void *ws, cudaStream_t s);
+
+}  // namespace ghn

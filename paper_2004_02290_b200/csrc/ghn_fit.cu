@@ -1,0 +1,485 @@
+// ghn_fit.cu -- grid build (fit) for sm_100a.
+//
+// Replaces grid.build (grid.py:165-195):
+//   K1 bounds   per-dim min/max of floor(x/w), origin = min coordinate,
+//               non-finite check (core.py:35-36)                 [HBM read n*d]
+//   K2 keys     row-major linear cell key over the id bounding box
+//               (dim 0 most significant == lexicographic order)   [read n*d, write 4n]
+//   K5 sort     stable LSD radix sort of (key, index)  == lexsort((arange, ids...))
+//   K6 cells    run boundaries -> cell_start / cell_ids (== cell_array, buckets)
+//   K4 dense    ne_off (non-empty prefix) and pt_off (slot prefix) over E cells
+//   gather      permuted SoA coordinates coords[j*n + slot]
+// LIST layout (huge sparse boxes): one stable radix sort per dimension,
+// last dimension first (the lexsort key order), no dense tables.
+#include <math.h>
+#include <stdio.h>
+#include <string.h>
+
+#include "ghn_common.cuh"
+
+namespace ghn {
+namespace {
+
+constexpr int FIT_THREADS = 256;
+
+struct DimParams {
+    double w[GHN_MAX_DIM];
+    double inv[GHN_MAX_DIM];
+    int64_t lo[GHN_MAX_DIM];
+    int64_t ext[GHN_MAX_DIM];
+    uint32_t pow2;   // bit j: widths[j] is a power of two
+    int32_t d;
+};
+
+static DimParams make_dims(int d, const double *widths, const int64_t *lo, const int64_t *ext) {
+    DimParams p;
+    memset(&p, 0, sizeof(p));
+    p.d = d;
+    for (int j = 0; j < d; ++j) {
+        p.w[j] = widths[j];
+        double inv = 0.0;
+        if (is_pow2_width(widths[j], &inv)) {
+            p.pow2 |= 1u << j;
+            p.inv[j] = inv;
+        }
+        if (lo) p.lo[j] = lo[j];
+        if (ext) p.ext[j] = ext[j];
+    }
+    return p;
+}
+
+__global__ void bounds_init_kernel(int64_t *bounds, unsigned long long *origin_key, int32_t *flags,
+                                   int d) {
+    int j = threadIdx.x;
+    if (j < d) {
+        bounds[j] = INT64_MAX;
+        bounds[d + j] = INT64_MIN;
+        origin_key[j] = ~0ull;
+    }
+    if (j == 0) *flags = 0;
+}
+
+// K1: D > 0 compile-time dims; one point per thread iteration.
+template <typename T, int D>
+__global__ void __launch_bounds__(FIT_THREADS) bounds_kernel(const T *__restrict__ X, int64_t n,
+                                                             DimParams p, int64_t *bounds,
+                                                             unsigned long long *origin_key,
+                                                             int32_t *flags) {
+    int64_t lo[D], hi[D];
+    double mn[D];
+    bool bad = false;
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+        lo[j] = INT64_MAX;
+        hi[j] = INT64_MIN;
+        mn[j] = INFINITY;
+    }
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+            double x = to_double(X[i * D + j]);
+            if (!isfinite(x)) {
+                bad = true;
+                continue;
+            }
+            int64_t c = cell_id(x, p.w[j], p.inv[j], (p.pow2 >> j) & 1u);
+            lo[j] = c < lo[j] ? c : lo[j];
+            hi[j] = c > hi[j] ? c : hi[j];
+            mn[j] = fmin(mn[j], x);
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+        int64_t l = warp_min(lo[j]);
+        int64_t h = warp_max(hi[j]);
+        double m = mn[j];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) m = fmin(m, __shfl_xor_sync(GHN_FULL, m, o));
+        if ((threadIdx.x & 31) == 0) {
+            atomicMin((long long *)&bounds[j], (long long)l);
+            atomicMax((long long *)&bounds[D + j], (long long)h);
+            if (m != INFINITY) atomicMin(&origin_key[j], dbl_order_key(m));
+        }
+    }
+    if (__any_sync(GHN_FULL, bad) && (threadIdx.x & 31) == 0) atomicOr(flags, 1);
+}
+
+// K1 for runtime d (up to GHN_MAX_DIM): element-parallel with global atomics per warp-run.
+template <typename T>
+__global__ void __launch_bounds__(FIT_THREADS) bounds_kernel_rt(const T *__restrict__ X, int64_t n,
+                                                                DimParams p, int64_t *bounds,
+                                                                unsigned long long *origin_key,
+                                                                int32_t *flags) {
+    const int d = p.d;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        for (int j = 0; j < d; ++j) {
+            double x = to_double(X[i * d + j]);
+            if (!isfinite(x)) {
+                atomicOr(flags, 1);
+                continue;
+            }
+            int64_t c = cell_id(x, p.w[j], p.inv[j], (p.pow2 >> j) & 1u);
+            atomicMin((long long *)&bounds[j], (long long)c);
+            atomicMax((long long *)&bounds[d + j], (long long)c);
+            atomicMin(&origin_key[j], dbl_order_key(x));
+        }
+    }
+}
+
+__global__ void origin_decode_kernel(const unsigned long long *origin_key, double *origin, int d) {
+    int j = threadIdx.x;
+    if (j < d) origin[j] = dbl_from_order_key(origin_key[j]);
+}
+
+// K2: linear key over the bbox, row-major with dim 0 most significant.
+template <typename T>
+__global__ void __launch_bounds__(FIT_THREADS) linear_key_kernel(const T *__restrict__ X, int64_t n,
+                                                                 DimParams p,
+                                                                 uint32_t *__restrict__ keys) {
+    const int d = p.d;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        uint64_t key = 0;
+        for (int j = 0; j < d; ++j) {
+            int64_t c = cell_id(to_double(X[i * d + j]), p.w[j], p.inv[j], (p.pow2 >> j) & 1u);
+            key = key * (uint64_t)p.ext[j] + (uint64_t)(c - p.lo[j]);
+        }
+        keys[i] = (uint32_t)key;
+    }
+}
+
+// LIST layout: relative id of dimension j for the point at slot i of perm.
+template <typename T>
+__global__ void __launch_bounds__(FIT_THREADS) dim_key_kernel(const T *__restrict__ X, int64_t n,
+                                                              DimParams p, int j,
+                                                              const int32_t *__restrict__ perm,
+                                                              uint32_t *__restrict__ keys) {
+    const int d = p.d;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        int64_t src = perm ? perm[i] : i;
+        int64_t c = cell_id(to_double(X[src * d + j]), p.w[j], p.inv[j], (p.pow2 >> j) & 1u);
+        keys[i] = (uint32_t)(c - p.lo[j]);
+    }
+}
+
+// K6 (DENSE): boundary flags from sorted linear keys.
+__global__ void dense_flags_kernel(const uint32_t *__restrict__ skeys, int64_t n, int32_t *flags) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        flags[i] = (i == 0 || skeys[i] != skeys[i - 1]) ? 1 : 0;
+}
+
+__global__ void dense_emit_kernel(const uint32_t *__restrict__ skeys, int64_t n,
+                                  const int32_t *__restrict__ cidx, DimParams p,
+                                  int32_t *__restrict__ cell_start, int32_t *__restrict__ cell_ids,
+                                  int32_t *__restrict__ n_cells, int32_t *__restrict__ ne_flag) {
+    const int d = p.d;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        bool head = (i == 0 || skeys[i] != skeys[i - 1]);
+        if (head) {
+            int32_t c = cidx[i];
+            cell_start[c] = (int32_t)i;
+            uint64_t rem = skeys[i];
+            for (int j = d - 1; j >= 0; --j) {
+                cell_ids[(int64_t)c * d + j] = (int32_t)(rem % (uint64_t)p.ext[j]);
+                rem /= (uint64_t)p.ext[j];
+            }
+            if (ne_flag) ne_flag[skeys[i]] = 1;
+        }
+        if (i == n - 1) {
+            int32_t total = cidx[i] + 1;
+            *n_cells = total;
+            cell_start[total] = (int32_t)n;
+        }
+    }
+}
+
+// K6 (LIST): boundary flags by comparing the id tuples of consecutive slots.
+template <typename T>
+__global__ void list_flags_kernel(const T *__restrict__ X, int64_t n, DimParams p,
+                                  const int32_t *__restrict__ perm, int32_t *flags) {
+    const int d = p.d;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        int f = 0;
+        if (i == 0) {
+            f = 1;
+        } else {
+            int64_t a = perm[i], b = perm[i - 1];
+            for (int j = 0; j < d; ++j) {
+                bool pw = (p.pow2 >> j) & 1u;
+                if (cell_id(to_double(X[a * d + j]), p.w[j], p.inv[j], pw) !=
+                    cell_id(to_double(X[b * d + j]), p.w[j], p.inv[j], pw)) {
+                    f = 1;
+                    break;
+                }
+            }
+        }
+        flags[i] = f;
+    }
+}
+
+template <typename T>
+__global__ void list_emit_kernel(const T *__restrict__ X, int64_t n, DimParams p,
+                                 const int32_t *__restrict__ perm, const int32_t *__restrict__ cidx,
+                                 int32_t *__restrict__ cell_start, int32_t *__restrict__ cell_ids,
+                                 int32_t *__restrict__ n_cells) {
+    const int d = p.d;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        int32_t c = cidx[i];
+        int32_t cnext = (i + 1 < n) ? cidx[i + 1] : -1;
+        bool head = (i == 0) || (cidx[i - 1] != c);
+        (void)cnext;
+        if (head) {
+            cell_start[c] = (int32_t)i;
+            int64_t a = perm[i];
+            for (int j = 0; j < d; ++j) {
+                int64_t id = cell_id(to_double(X[a * d + j]), p.w[j], p.inv[j], (p.pow2 >> j) & 1u);
+                cell_ids[(int64_t)c * d + j] = (int32_t)(id - p.lo[j]);
+            }
+        }
+        if (i == n - 1) {
+            *n_cells = c + 1;
+            cell_start[c + 1] = (int32_t)n;
+        }
+    }
+}
+
+// inclusive-to-cell-index: cidx[i] = (# heads in [0, i]) - 1, from an exclusive scan of flags.
+__global__ void excl_to_cidx_kernel(const int32_t *__restrict__ flags_excl,
+                                    const int32_t *__restrict__ flags, int32_t *cidx, int64_t n) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        cidx[i] = flags_excl[i] + flags[i] - 1;
+}
+
+// K4 (DENSE): pt_off[c] = cell_start[ne_off[c]] for c in [0, E].
+__global__ void pt_off_kernel(const int32_t *__restrict__ ne_off, const int32_t *__restrict__ cell_start,
+                              int32_t *__restrict__ pt_off, int64_t len) {
+    for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < len;
+         c += (int64_t)gridDim.x * blockDim.x)
+        pt_off[c] = cell_start[ne_off[c]];
+}
+
+// Permuted SoA coordinates.
+template <typename T>
+__global__ void __launch_bounds__(FIT_THREADS) gather_coords_kernel(const T *__restrict__ X, int64_t n,
+                                                                    int d,
+                                                                    const int32_t *__restrict__ perm,
+                                                                    T *__restrict__ out) {
+    for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < n;
+         s += (int64_t)gridDim.x * blockDim.x) {
+        int64_t src = perm[s];
+        for (int j = 0; j < d; ++j) out[(int64_t)j * n + s] = X[src * d + j];
+    }
+}
+
+static unsigned grid_for(int64_t n, int threads = FIT_THREADS) {
+    int64_t b = (n + threads - 1) / threads;
+    int64_t cap = 148LL * 16;
+    if (b > cap) b = cap;
+    if (b < 1) b = 1;
+    return (unsigned)b;
+}
+
+static int bits_for(uint64_t maxval) {
+    int b = 0;
+    while (b < 64 && (maxval >> b) != 0) ++b;
+    return b;
+}
+
+static size_t align256(size_t b) { return (b + 255) & ~(size_t)255; }
+
+template <typename T>
+int32_t bounds_launch(const T *X, int64_t n, int d, const DimParams &p, int64_t *bounds,
+                      unsigned long long *okey, int32_t *flags, cudaStream_t s) {
+    unsigned g = grid_for(n);
+    switch (d) {
+#define GHN_BCASE(DD) \
+    case DD: bounds_kernel<T, DD><<<g, FIT_THREADS, 0, s>>>(X, n, p, bounds, okey, flags); break;
+        GHN_BCASE(1) GHN_BCASE(2) GHN_BCASE(3) GHN_BCASE(4)
+        GHN_BCASE(5) GHN_BCASE(6) GHN_BCASE(7) GHN_BCASE(8)
+#undef GHN_BCASE
+        default: bounds_kernel_rt<T><<<g, FIT_THREADS, 0, s>>>(X, n, p, bounds, okey, flags);
+    }
+    GHN_LAUNCH_CHECK("bounds_kernel");
+    return GHN_OK;
+}
+
+template <typename T>
+int32_t fit_build_impl(const ghn_fit_plan *plan, const T *X, const ghn_fit_out *out, char *ws,
+                       size_t ws_bytes, cudaStream_t s) {
+    const int64_t n = plan->n;
+    const int d = plan->d;
+    DimParams p = make_dims(d, plan->widths, plan->lo, plan->ext);
+    const size_t n4 = align256((size_t)n * 4);
+    uint32_t *kA = (uint32_t *)ws;
+    uint32_t *kB = (uint32_t *)(ws + n4);
+    uint32_t *kC = (uint32_t *)(ws + 2 * n4);
+    int32_t *vT = (int32_t *)(ws + 3 * n4);
+    int32_t *vP = (int32_t *)(ws + 4 * n4);
+    char *rws = ws + 5 * n4;
+    const size_t rws_bytes = align256(radix_workspace_bytes(n));
+    char *sws = rws + rws_bytes;
+    const unsigned g = grid_for(n);
+    int32_t rc;
+
+    if (plan->layout == GHN_LAYOUT_DENSE) {
+        linear_key_kernel<T><<<g, FIT_THREADS, 0, s>>>(X, n, p, kA);
+        GHN_LAUNCH_CHECK("linear_key_kernel");
+        rc = radix_sort_pairs(kA, nullptr, kB, out->perm, kC, vT, n, plan->key_bits, rws, s);
+        if (rc) return rc;
+        // kB = sorted keys; out->perm = order.  flags -> kA (as int32), cidx -> vT
+        int32_t *flags = (int32_t *)kA;
+        dense_flags_kernel<<<g, FIT_THREADS, 0, s>>>(kB, n, flags);
+        GHN_LAUNCH_CHECK("dense_flags_kernel");
+        rc = exclusive_scan_i32(flags, (int32_t *)kC, n, sws, s);
+        if (rc) return rc;
+        excl_to_cidx_kernel<<<g, FIT_THREADS, 0, s>>>((int32_t *)kC, flags, vT, n);
+        GHN_LAUNCH_CHECK("excl_to_cidx_kernel");
+        // ne flags live in ne_off before the scan
+        GHN_CUDA_CHECK(cudaMemsetAsync(out->ne_off, 0, (size_t)(plan->E + 1) * 4, s));
+        dense_emit_kernel<<<g, FIT_THREADS, 0, s>>>(kB, n, vT, p, out->cell_start, out->cell_ids,
+                                                   out->n_cells, out->ne_off);
+        GHN_LAUNCH_CHECK("dense_emit_kernel");
+        rc = exclusive_scan_i32(out->ne_off, out->ne_off, plan->E + 1, sws, s);
+        if (rc) return rc;
+        pt_off_kernel<<<grid_for(plan->E + 1), FIT_THREADS, 0, s>>>(out->ne_off, out->cell_start,
+                                                                    out->pt_off, plan->E + 1);
+        GHN_LAUNCH_CHECK("pt_off_kernel");
+    } else {
+        // LIST: stable sort by each dimension, least significant (last) first.
+        int32_t *cur = nullptr;       // nullptr = identity
+        int32_t *bufs[2] = {vP, out->perm};
+        int which = 0;
+        for (int j = d - 1; j >= 0; --j) {
+            dim_key_kernel<T><<<g, FIT_THREADS, 0, s>>>(X, n, p, j, cur, kA);
+            GHN_LAUNCH_CHECK("dim_key_kernel");
+            int32_t *dst = bufs[which];
+            rc = radix_sort_pairs(kA, cur, kB, dst, kC, vT, n, bits_for((uint64_t)(plan->ext[j] - 1)), rws, s);
+            if (rc) return rc;
+            cur = dst;
+            which ^= 1;
+        }
+        if (cur != out->perm) GHN_CUDA_CHECK(cudaMemcpyAsync(out->perm, cur, (size_t)n * 4, cudaMemcpyDeviceToDevice, s));
+        int32_t *flags = (int32_t *)kA;
+        list_flags_kernel<T><<<g, FIT_THREADS, 0, s>>>(X, n, p, out->perm, flags);
+        GHN_LAUNCH_CHECK("list_flags_kernel");
+        rc = exclusive_scan_i32(flags, (int32_t *)kC, n, sws, s);
+        if (rc) return rc;
+        excl_to_cidx_kernel<<<g, FIT_THREADS, 0, s>>>((int32_t *)kC, flags, vT, n);
+        GHN_LAUNCH_CHECK("excl_to_cidx_kernel");
+        list_emit_kernel<T><<<g, FIT_THREADS, 0, s>>>(X, n, p, out->perm, vT, out->cell_start,
+                                                       out->cell_ids, out->n_cells);
+        GHN_LAUNCH_CHECK("list_emit_kernel");
+    }
+    gather_coords_kernel<T><<<g, FIT_THREADS, 0, s>>>(X, n, d, out->perm, (T *)out->coords);
+    GHN_LAUNCH_CHECK("gather_coords_kernel");
+    (void)ws_bytes;
+    return GHN_OK;
+}
+
+}  // namespace
+}  // namespace ghn
+
+using namespace ghn;
+
+extern "C" int32_t ghn_fit_bounds(const void *X, int32_t dtype, int64_t n, int32_t d,
+                                  const double *widths, int64_t *out_bounds, double *out_origin,
+                                  int32_t *out_flags, void *stream) {
+    if (n <= 0) {
+        set_error("empty dataset");
+        return GHN_ERR_VALUE;
+    }
+    if (d < 1 || d > GHN_MAX_DIM) {
+        set_error("d=%d unsupported (1..%d)", d, GHN_MAX_DIM);
+        return GHN_ERR_UNSUPPORTED;
+    }
+    for (int j = 0; j < d; ++j) {
+        if (!(widths[j] > 0.0) || !isfinite(widths[j])) {
+            set_error("all cell widths must be positive");
+            return GHN_ERR_VALUE;
+        }
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    DimParams p = make_dims(d, widths, nullptr, nullptr);
+    // origin keys are staged in out_origin's bytes (same size as uint64)
+    unsigned long long *okey = (unsigned long long *)out_origin;
+    bounds_init_kernel<<<1, 32, 0, s>>>(out_bounds, okey, out_flags, d);
+    GHN_LAUNCH_CHECK("bounds_init_kernel");
+    int32_t rc = dtype == GHN_F32
+                     ? bounds_launch<float>((const float *)X, n, d, p, out_bounds, okey, out_flags, s)
+                     : bounds_launch<double>((const double *)X, n, d, p, out_bounds, okey, out_flags, s);
+    if (rc) return rc;
+    origin_decode_kernel<<<1, 32, 0, s>>>(okey, out_origin, d);
+    GHN_LAUNCH_CHECK("origin_decode_kernel");
+    return GHN_OK;
+}
+
+extern "C" int32_t ghn_fit_plan_init(ghn_fit_plan *plan, int64_t n, int32_t d, int32_t dtype,
+                                     const double *widths, const int64_t *bounds_host,
+                                     int64_t dense_limit) {
+    memset(plan, 0, sizeof(*plan));
+    if (n <= 0 || n > 0x7ffffffeLL) {
+        set_error("n=%lld out of range", (long long)n);
+        return n <= 0 ? GHN_ERR_VALUE : GHN_ERR_UNSUPPORTED;
+    }
+    if (d < 1 || d > GHN_MAX_DIM) {
+        set_error("d=%d unsupported", d);
+        return GHN_ERR_UNSUPPORTED;
+    }
+    plan->n = n;
+    plan->d = d;
+    plan->dtype = dtype;
+    double Ed = 1.0;
+    for (int j = 0; j < d; ++j) {
+        plan->widths[j] = widths[j];
+        plan->lo[j] = bounds_host[j];
+        int64_t hi = bounds_host[d + j];
+        if (hi < plan->lo[j]) {
+            set_error("bounds not computed");
+            return GHN_ERR_VALUE;
+        }
+        plan->ext[j] = hi - plan->lo[j] + 1;
+        if (plan->ext[j] > 0x7fffffffLL || plan->ext[j] <= 0) {
+            set_error("grid extent %lld along dim %d exceeds the int32 id range", (long long)plan->ext[j], j);
+            return GHN_ERR_UNSUPPORTED;
+        }
+        Ed *= (double)plan->ext[j];
+    }
+    if (dense_limit > (1LL << 31)) dense_limit = 1LL << 31;
+    if (Ed <= (double)dense_limit) {
+        plan->layout = GHN_LAYOUT_DENSE;
+        plan->E = (int64_t)Ed;
+        plan->key_bits = bits_for((uint64_t)(plan->E - 1));
+    } else {
+        plan->layout = GHN_LAYOUT_LIST;
+        plan->E = 0;
+    }
+    size_t n4 = align256((size_t)n * 4);
+    size_t scan_len = (size_t)n + 1;
+    if (plan->layout == GHN_LAYOUT_DENSE && (size_t)plan->E + 1 > scan_len) scan_len = plan->E + 1;
+    plan->workspace_bytes = 5 * n4 + align256(radix_workspace_bytes(n)) + scan_workspace_bytes(scan_len) + 256;
+    return GHN_OK;
+}
+
+extern "C" int32_t ghn_fit_build(const ghn_fit_plan *plan, const void *X, const ghn_fit_out *out,
+                                 void *workspace, size_t workspace_bytes, void *stream) {
+    if (workspace_bytes < plan->workspace_bytes) {
+        set_error("workspace too small: %zu < %zu", workspace_bytes, plan->workspace_bytes);
+        return GHN_ERR_VALUE;
+    }
+    if (plan->layout == GHN_LAYOUT_DENSE && (!out->pt_off || !out->ne_off)) {
+        set_error("DENSE layout needs pt_off and ne_off");
+        return GHN_ERR_VALUE;
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    if (plan->dtype == GHN_F32)
+        return fit_build_impl<float>(plan, (const float *)X, out, (char *)workspace, workspace_bytes, s);
+    return fit_build_impl<double>(plan, (const double *)X, out, (char *)workspace, workspace_bytes, s);
+}
