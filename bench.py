@@ -1,0 +1,461 @@
+#!/usr/bin/env python
+"""GHN bench: BASELINE.json's metric on config 4 (2-D, 100M points, 10M
+queries, C=4096, k sweep {1,4,16,64}, majority vote) on 1..N B200s.
+
+One step = one batched predict of all nq queries for every k of the sweep
+(4 x nq queries), inputs resident in HBM.  Per k: query binning
+(ghn_query_order) + the predict kernel (ghn_query), timed with CUDA events
+on the launching stream.  The training data (800 MB) and the CSR tables
+exceed L2 (126 MB) and L2 is also flushed between steps.
+
+  value     whole-job queries/s (sum over ranks, max-over-ranks time)
+  e2e       same metric through predict_batch with HOST (pinned) queries:
+            H2D of the queries and D2H of the labels inside the timed region
+  roofline  predict kernel: algorithmic bytes (4d(1+S_q) + 4
+            per query, S_q = points scanned) / kernel time vs measured HBM peak
+  fit       grid build (fit) points/s, device-resident input
+  cpu_baseline  the oracle port (numpy restatement of the reference
+            algorithm) on a bounded query sample on this host
+
+Multi-GPU (--gpus N under torchrun): replicas -- every rank builds the same
+index and predicts its own 10M-query shard (weak scaling, no data-path
+collective); barrier + max-over-ranks device time.
+
+`--impl reference` times the reference algorithm (oracle/ghn_port.py) on the
+host cores instead, on the same config (rank 0 only).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+FLUSH_BYTES = 512 << 20     # > 126 MB L2
+
+
+def parse_args(argv=None):
+    ap = argparse.ArgumentParser(description=__doc__.split("\n")[0])
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--config", type=int, default=4)
+    ap.add_argument("--ks", type=str, default=None, help="k sweep, default: the config's")
+    ap.add_argument("--n", type=int, default=None, help="override n_train (debug only)")
+    ap.add_argument("--nq", type=int, default=None, help="override queries per rank (debug only)")
+    ap.add_argument("--cpu-sample", type=int, default=1, help="port queries per k for cpu_baseline")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args(argv)
+
+
+def peaks():
+    p = os.path.join(REPO, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as fh:
+            m = json.load(fh)
+        return float(m["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def ncu_traffic(cfg, ks):
+    """Per-launch DRAM bytes of the predict kernel from the committed ncu summary."""
+    p = os.path.join(REPO, "profiles", "ncu_summary.json")
+    try:
+        with open(p) as fh:
+            m = json.load(fh)
+        per = m[f"cfg{cfg}"]["query_kernel_dram_bytes_per_launch"]
+        vals = [per[str(k)] for k in ks if str(k) in per]
+        return sum(vals) / len(vals) if len(vals) == len(ks) else None
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        rows = []
+        try:
+            with open(self.path) as fh:
+                for line in fh:
+                    parts = [x.strip() for x in line.split(",")]
+                    if len(parts) >= 9:
+                        rows.append(parts)
+        except Exception:
+            pass
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+def dist_setup():
+    import torch
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        backend = "nccl" if torch.cuda.is_available() else "gloo"
+        if backend == "nccl":
+            torch.cuda.set_device(local)
+        dist.init_process_group(backend)
+    elif torch.cuda.is_available():
+        torch.cuda.set_device(local)
+    return rank, world, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+def max_over_ranks(x, world):
+    if world <= 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([x], dtype=torch.float64, device="cuda" if torch.cuda.is_available() else "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ------------------------------------------------------------------ CPU legs
+def port_index(w):
+    """Oracle port index for the workload (arrays from the pinned C restatement)."""
+    import oracle
+    from oracle import ghn_port
+
+    c = oracle.COracle(w.X, w.widths)
+    order, cids, starts, _, _ = c.export()
+    return ghn_port.PortIndex.from_arrays(w.X, w.y, w.widths, order, starts, cids), c
+
+
+def _port_worker(args):
+    from oracle import ghn_port
+
+    qs, k = args
+    ix = _PORT_IX
+    for q in qs:
+        keys, idx, _ = ghn_port.knn(ix, q, k)
+        ghn_port.classify(keys, idx, ix.labels)
+    return len(qs)
+
+
+_PORT_IX = None
+
+
+def port_queries_per_s(ix, Q, ks, per_k, procs):
+    """Time the port's knn + classify over per_k queries per k with `procs` processes."""
+    global _PORT_IX
+    _PORT_IX = ix
+    total = 0
+    t0 = time.perf_counter()
+    if procs <= 1:
+        for k in ks:
+            total += _port_worker((Q[:per_k], k))
+    else:
+        import multiprocessing as mp
+
+        ctx = mp.get_context("fork")
+        jobs = []
+        for k in ks:
+            for p in range(procs):
+                qs = Q[p * per_k:(p + 1) * per_k]
+                if len(qs):
+                    jobs.append((qs, k))
+        with ctx.Pool(procs) as pool:
+            total = sum(pool.map(_port_worker, jobs, chunksize=1))
+    return total / (time.perf_counter() - t0), total
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+# ------------------------------------------------------------------ arms
+def run_reference(args):
+    rank, world, _ = (int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")), 0)
+    if rank != 0:
+        return 0
+    from paper_2004_02290_b200 import datagen
+
+    cfg = args.config
+    w = datagen.make(cfg, n=args.n, nq=args.nq)
+    ks = [int(x) for x in args.ks.split(",")] if args.ks else (list(w.ks) or [w.k])
+    ix, _ = port_index(w)
+    procs = os.cpu_count() or 1
+    per_k = 1
+    # warmup (untimed) then K timed steps, each a bounded sample: `procs` queries per k
+    for _ in range(max(0, min(args.warmup, 1))):
+        port_queries_per_s(ix, w.Q, ks[:1], 1, 1)
+    rates, done = [], 0
+    t_all = time.perf_counter()
+    for s in range(args.steps):
+        Qs = w.Q[(s * procs * per_k) % max(1, w.Q.shape[0] - procs * per_k):][: procs * per_k]
+        r, cnt = port_queries_per_s(ix, Qs, ks, per_k, procs)
+        rates.append(r)
+        done += cnt
+    wall = time.perf_counter() - t_all
+    value = done / wall
+    line = {
+        "impl": "reference",
+        "metric": "GHN kNN predict queries/s (k sweep, majority vote)",
+        "value": value, "unit": "queries/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * wall / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"cfg{cfg}: {w.X.shape[0]} x {w.X.shape[1]}-D uniform, C={w.cells_per_axis}, "
+                               f"k sweep {ks}, vote", "n_train": int(w.X.shape[0]),
+                   "queries_per_step": len(ks) * procs * per_k, "k_sweep": ks},
+        "cpu_baseline": {"value": value, "unit": "queries/s", "cores": procs, "kind": "port",
+                         "sample": f"{procs * per_k} queries per k per step x {len(ks)} k, "
+                                   f"{args.steps} steps; oracle/ghn_port.py (reference algorithm, "
+                                   f"O(#cells) scans) forked over {procs} processes; {cpu_model()}"},
+        "e2e": {"value": value, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_ours(args):
+    import numpy as np
+    import torch
+
+    from paper_2004_02290_b200 import _lib, build_arrays, datagen, predict_batch, query_order
+
+    rank, world, local = dist_setup()
+    dev = torch.device("cuda", torch.cuda.current_device())
+    cfg = args.config
+    # replicas: identical training data on every rank, a distinct query shard per rank
+    w = datagen.make(cfg, n=args.n, nq=args.nq)
+    if rank > 0:
+        rng = np.random.default_rng(1000 + rank)
+        w.Q = rng.random(w.Q.shape, dtype=np.float32)
+    ks = [int(x) for x in args.ks.split(",")] if args.ks else (list(w.ks) or [w.k])
+    n, d = w.X.shape
+    nq = w.Q.shape[0]
+    L = _lib.lib()
+    X_d = torch.from_numpy(w.X).to(dev)
+    y_d = torch.from_numpy(w.y).to(dev)
+    Q_d = torch.from_numpy(w.Q).to(dev)
+    flush = torch.empty(FLUSH_BYTES, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream()
+
+    # ---- fit (grid build): points/s, device-resident input
+    index = build_arrays(X_d, y_d, cells_per_axis=w.cells_per_axis)
+    fit_ms = []
+    for _ in range(2):
+        flush.zero_()
+        del index
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        index = build_arrays(X_d, y_d, cells_per_axis=w.cells_per_axis)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        fit_ms.append(e0.elapsed_time(e1))
+    fit_s = min(fit_ms) / 1e3
+
+    # ---- algorithmic bytes per k (untimed, deterministic): S_q from the device counters
+    scanned = {}
+    for k in ks:
+        r = predict_batch(index, Q_d, k, totals=True, confidence=False)
+        tot = r["totals"].cpu().numpy()
+        scanned[k] = {"layers": int(tot[0]), "cells": int(tot[1]), "points": int(tot[2])}
+    algo_bytes = {k: 4 * d * (nq + scanned[k]["points"]) + 4 * nq for k in ks}
+
+    def step(timed):
+        ev = []
+        for k in ks:
+            e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+            e0.record(stream)
+            order = query_order(index, Q_d)
+            e1.record(stream)
+            predict_batch(index, Q_d, k, qorder=order, confidence=False)
+            e2.record(stream)
+            ev.append((k, e0, e1, e2))
+        return ev
+
+    for _ in range(args.warmup):
+        flush.zero_()
+        step(False)
+    torch.cuda.synchronize()
+    per_k_total = {k: 0.0 for k in ks}
+    per_k_kernel = {k: 0.0 for k in ks}
+    launches0 = int(L.ghn_launch_count())
+    with ClockSampler(local) as clocks:
+        for _ in range(args.steps):
+            flush.zero_()
+            barrier(world)
+            torch.cuda.synchronize()
+            evs = step(True)
+            torch.cuda.synchronize()
+            barrier(world)
+            for k, e0, e1, e2 in evs:
+                per_k_total[k] += e0.elapsed_time(e2)
+                per_k_kernel[k] += e1.elapsed_time(e2)
+    launches = int(L.ghn_launch_count()) - launches0
+    step_ms = sum(per_k_total.values()) / args.steps
+    step_ms_max = max_over_ranks(step_ms, world)
+    queries_per_step = len(ks) * nq
+    value = world * queries_per_step / (step_ms_max / 1e3)
+    kernel_s = sum(per_k_kernel.values()) / args.steps / 1e3
+    achieved = sum(algo_bytes.values()) / kernel_s / 1e9
+    peak, peak_kind = peaks()
+    per_k = {str(k): {"queries_per_s": nq / (per_k_total[k] / args.steps / 1e3),
+                      "kernel_ms": per_k_kernel[k] / args.steps,
+                      "binning_ms": (per_k_total[k] - per_k_kernel[k]) / args.steps,
+                      "mean_points_scanned": scanned[k]["points"] / nq,
+                      "mean_layers": scanned[k]["layers"] / nq,
+                      "algo_GBps": algo_bytes[k] / (per_k_kernel[k] / args.steps / 1e3) / 1e9}
+             for k in ks}
+
+    # ---- e2e through the public API with host buffers
+    e2e = None
+    if not args.no_e2e:
+        Q_h = torch.from_numpy(w.Q).pin_memory()
+        lab_h = torch.empty(nq, dtype=torch.int32).pin_memory()
+        def e2e_step():
+            for k in ks:
+                Qd = Q_h.to(dev, non_blocking=True)
+                r = predict_batch(index, Qd, k, confidence=False)
+                lab_h.copy_(r["label"], non_blocking=True)
+        e2e_step()
+        torch.cuda.synchronize()
+        e2e_ms = 0.0
+        for _ in range(args.steps):
+            flush.zero_()
+            barrier(world)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            e2e_step()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            e2e_ms += e0.elapsed_time(e1)
+        e2e_ms = max_over_ranks(e2e_ms / args.steps, world)
+        e2e = {"value": world * queries_per_step / (e2e_ms / 1e3), "unit": "queries/s",
+               "h2d_bytes_per_step": len(ks) * int(Q_h.numel() * 4),
+               "d2h_bytes_per_step": len(ks) * int(lab_h.numel() * 4), "ms_per_step": e2e_ms}
+
+    # ---- CPU legs (rank 0, N=1 only)
+    cpu_baseline = None
+    cpu_c = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        pix, cor = port_index(w)
+        per = max(1, args.cpu_sample)
+        v, cnt = port_queries_per_s(pix, w.Q, ks, per, 1)
+        cpu_baseline = {"value": v, "unit": "queries/s", "cores": 1, "kind": "port",
+                        "sample": f"{per} queries x k in {ks} through oracle/ghn_port.py (reference "
+                                  f"algorithm: O(#cells)={index.n_cells} scan per query and layer) "
+                                  f"+ vote; {cpu_model()}"}
+        th = os.cpu_count() or 1
+        m = min(nq, 200000)
+        t0 = time.perf_counter()
+        for k in ks:
+            keys, idx, _ = cor.query(w.Q[:m], k, threads=th)
+        cpu_c = {"value": len(ks) * m / (time.perf_counter() - t0), "unit": "queries/s", "cores": th,
+                 "sample": f"{m} queries x k in {ks}, oracle/ghn_oracle.c (dense ring enumeration, "
+                           f"OpenMP), neighbours only"}
+
+    if rank == 0:
+        line = {
+            "metric": "GHN kNN predict queries/s (k sweep, majority vote)",
+            "value": value, "unit": "queries/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": step_ms_max, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"cfg{cfg}: {n} x {d}-D uniform fp32, {nq} queries/rank, "
+                                   f"C={w.cells_per_axis}, k sweep {ks}, heuristic stop, vote",
+                       "n_train": n, "queries_per_rank": nq, "k_sweep": ks,
+                       "cells_nonempty": index.n_cells, "layout": index.layout,
+                       "l2": "flushed between steps (512 MB write); data 800 MB > L2",
+                       "storage": "coords fp32 SoA, keys fp64 (numpy einsum order)",
+                       "parallelism": f"replicas x{world} (query shards)"},
+            "fit": {"points_per_s": n / fit_s, "ms": fit_s * 1e3, "unit": "points/s"},
+            "per_k": per_k,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "peak_kind": peak_kind,
+                         "traffic": ncu_traffic(cfg, ks),
+                         "kernel": "query_kernel (ghn_query)",
+                         "algorithmic_bytes_per_step": sum(algo_bytes.values())},
+            "e2e": e2e,
+            "gpu_launches": launches // args.steps,
+            "gpu_launches_total": launches,
+            "clocks": clocks.summary(),
+            "cpu_baseline": cpu_baseline,
+            "cpu_c_oracle": cpu_c,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+    return 0
+
+
+def main(argv=None):
+    args = parse_args(argv)
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

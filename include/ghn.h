@@ -130,12 +130,24 @@ typedef struct ghn_query_out {
 /* Workspace for query binning (sorting queries by their central cell). */
 size_t ghn_query_workspace_size(const ghn_index_view *ix, int64_t nq);
 
+/* K8 query binning (new; the reference loops per query, bench.py:194):
+ * order_out[t] = query visited t-th, sorted by central cell (DENSE layout;
+ * returns GHN_ERR_UNSUPPORTED for LIST).  Any order gives identical
+ * results; this one makes warps on an SM share neighbourhoods. */
+int32_t ghn_query_order(const ghn_index_view *ix, const void *Q, int32_t q_dtype, int64_t nq,
+                        int32_t *order_out, void *workspace, size_t workspace_bytes, void *stream);
+
 /* Q is (nq, d) row-major, dtype q_dtype (GHN_F32 / GHN_F64, independent of
  * the index dtype: queries are upcast to fp64 like explore.py:83).
- * 1 <= k <= n and k <= 256. */
-int32_t ghn_query(const ghn_index_view *ix, const void *Q, int32_t q_dtype, int64_t nq, int32_t k, int32_t mode,
-                  int32_t task, const ghn_query_out *out, void *workspace, size_t workspace_bytes,
-                  void *stream);
+ * 1 <= k <= n and k <= 256.  qorder: visit order from ghn_query_order, or
+ * NULL to bin internally (when nq is large enough to benefit). */
+int32_t ghn_query(const ghn_index_view *ix, const void *Q, int32_t q_dtype, int64_t nq, int32_t k,
+                  int32_t mode, int32_t task, const int32_t *qorder, const ghn_query_out *out,
+                  void *workspace, size_t workspace_bytes, void *stream);
+
+/* Number of kernels this library has launched in this process (evidence for
+ * the bench's gpu_launches; monotone, thread-safe). */
+uint64_t ghn_launch_count(void);
 
 #ifdef __cplusplus
 }

@@ -98,6 +98,23 @@ class PortIndex:
         self.cell_array = sid[self.starts]
         self.ends = np.append(self.starts[1:], n)
 
+    @classmethod
+    def from_arrays(cls, X, labels, widths, order, starts, cell_array):
+        """Assemble from (order, starts, cell_array) produced elsewhere -- the C
+        restatement, whose arrays tests/test_oracle.py pins equal to this
+        class's lexsort build.  Lets bench.py time knn() at 100M points without
+        a 200 s lexsort."""
+        self = cls.__new__(cls)
+        self.X = np.asarray(X, dtype=np.float64)
+        self.labels = np.asarray(labels)
+        self.widths = np.asarray(widths, dtype=np.float64)
+        self.order = np.asarray(order, dtype=np.int64)
+        st = np.asarray(starts, dtype=np.int64)
+        self.starts = st[:-1]
+        self.ends = st[1:]
+        self.cell_array = np.asarray(cell_array, dtype=np.int64)
+        return self
+
     @property
     def size(self):
         return self.X.shape[0]

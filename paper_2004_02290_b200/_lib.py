@@ -28,7 +28,9 @@ EXPORTS = (
     "ghn_fit_plan_init",
     "ghn_fit_build",
     "ghn_query_workspace_size",
+    "ghn_query_order",
     "ghn_query",
+    "ghn_launch_count",
 )
 
 _i64, _i32, _f64, _p, _sz = ctypes.c_int64, ctypes.c_int32, ctypes.c_double, ctypes.c_void_p, ctypes.c_size_t
@@ -98,9 +100,12 @@ def lib():
     L.ghn_fit_build.restype = _i32
     L.ghn_query_workspace_size.argtypes = [ctypes.POINTER(IndexView), _i64]
     L.ghn_query_workspace_size.restype = _sz
-    L.ghn_query.argtypes = [ctypes.POINTER(IndexView), _p, _i32, _i64, _i32, _i32, _i32,
+    L.ghn_query.argtypes = [ctypes.POINTER(IndexView), _p, _i32, _i64, _i32, _i32, _i32, _p,
                             ctypes.POINTER(QueryOut), _p, _sz, _p]
     L.ghn_query.restype = _i32
+    L.ghn_query_order.argtypes = [ctypes.POINTER(IndexView), _p, _i32, _i64, _p, _p, _sz, _p]
+    L.ghn_query_order.restype = _i32
+    L.ghn_launch_count.restype = ctypes.c_uint64
     _lib = L
     return L
 

@@ -20,8 +20,11 @@ int32_t cuda_status(cudaError_t e, const char *where);
         if (_e != cudaSuccess) return ::ghn::cuda_status(_e, #expr);   \
     } while (0)
 
+void count_launch();
+
 #define GHN_LAUNCH_CHECK(where)                                        \
     do {                                                               \
+        ::ghn::count_launch();                                         \
         cudaError_t _e = cudaGetLastError();                           \
         if (_e != cudaSuccess) return ::ghn::cuda_status(_e, where);   \
     } while (0)

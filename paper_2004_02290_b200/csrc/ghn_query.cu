@@ -591,9 +591,7 @@ extern "C" size_t ghn_query_workspace_size(const ghn_index_view *ix, int64_t nq)
     return a256(sizeof(BinConsts)) + 5 * q4 + a256(radix_workspace_bytes(nq > 0 ? nq : 1)) + 256;
 }
 
-extern "C" int32_t ghn_query(const ghn_index_view *ix, const void *Q, int32_t q_dtype, int64_t nq, int32_t k,
-                             int32_t mode, int32_t task, const ghn_query_out *out, void *workspace,
-                             size_t workspace_bytes, void *stream) {
+static int32_t validate_query(const ghn_index_view *ix, int32_t k, int32_t mode) {
     if (mode != GHN_MODE_HEURISTIC && mode != GHN_MODE_GUARANTEED) {
         set_error("unknown mode %d", mode);
         return GHN_ERR_VALUE;
@@ -610,18 +608,80 @@ extern "C" int32_t ghn_query(const ghn_index_view *ix, const void *Q, int32_t q_
         set_error("d=%d unsupported", ix->d);
         return GHN_ERR_UNSUPPORTED;
     }
+    return GHN_OK;
+}
+
+static uint32_t pow2_mask(const ghn_index_view *ix, double *inv_w) {
+    uint32_t m = 0;
+    for (int j = 0; j < ix->d; ++j) {
+        double inv = 0.0;
+        if (is_pow2_width(ix->widths[j], &inv)) {
+            m |= 1u << j;
+            inv_w[j] = inv;
+        }
+    }
+    return m;
+}
+
+extern "C" int32_t ghn_query_order(const ghn_index_view *ix, const void *Q, int32_t q_dtype,
+                                   int64_t nq, int32_t *order_out, void *workspace,
+                                   size_t workspace_bytes, void *stream) {
+    if (ix->layout != GHN_LAYOUT_DENSE) {
+        set_error("query binning needs the DENSE layout");
+        return GHN_ERR_UNSUPPORTED;
+    }
+    if (nq <= 0) return GHN_OK;
+    if (!workspace || workspace_bytes < ghn_query_workspace_size(ix, nq)) {
+        set_error("query workspace too small");
+        return GHN_ERR_VALUE;
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    char *ws = (char *)workspace;
+    BinConsts bc;
+    memset(&bc, 0, sizeof(bc));
+    const uint32_t pow2 = pow2_mask(ix, bc.inv);
+    for (int j = 0; j < ix->d; ++j) {
+        bc.w[j] = ix->widths[j];
+        bc.lo[j] = ix->lo[j];
+        bc.ext[j] = ix->ext[j];
+    }
+    BinConsts *dbc = (BinConsts *)ws;
+    GHN_CUDA_CHECK(cudaMemcpyAsync(dbc, &bc, sizeof(bc), cudaMemcpyHostToDevice, s));
+    const size_t q4 = a256((size_t)nq * 4);
+    char *p = ws + a256(sizeof(BinConsts));
+    uint32_t *kin = (uint32_t *)p;
+    uint32_t *kout = (uint32_t *)(p + q4);
+    uint32_t *ktmp = (uint32_t *)(p + 2 * q4);
+    int32_t *vtmp = (int32_t *)(p + 3 * q4);
+    char *rws = p + 5 * q4;
+    const int kb = bits_of((uint64_t)(ix->E > 0 ? ix->E - 1 : 0));
+    int keep = bits_of((uint64_t)nq) + 2;
+    if (keep > 24) keep = 24;
+    const int drop = kb > keep ? kb - keep : 0;
+    unsigned g = (unsigned)((nq + 255) / 256);
+    if (g > 148 * 16) g = 148 * 16;
+    if (q_dtype == GHN_F32)
+        query_bin_key_kernel<float><<<g, 256, 0, s>>>((const float *)Q, nq, ix->d, dbc->w, dbc->inv,
+                                                     pow2, dbc->lo, dbc->ext, drop, kin);
+    else
+        query_bin_key_kernel<double><<<g, 256, 0, s>>>((const double *)Q, nq, ix->d, dbc->w, dbc->inv,
+                                                      pow2, dbc->lo, dbc->ext, drop, kin);
+    GHN_LAUNCH_CHECK("query_bin_key_kernel");
+    return radix_sort_pairs(kin, nullptr, kout, order_out, ktmp, vtmp, nq, kb - drop, rws, s);
+}
+
+extern "C" int32_t ghn_query(const ghn_index_view *ix, const void *Q, int32_t q_dtype, int64_t nq,
+                             int32_t k, int32_t mode, int32_t task, const int32_t *qorder,
+                             const ghn_query_out *out, void *workspace, size_t workspace_bytes,
+                             void *stream) {
+    int32_t rc = validate_query(ix, k, mode);
+    if (rc) return rc;
     if (nq <= 0) return GHN_OK;
     cudaStream_t s = (cudaStream_t)stream;
     QArgs a;
     memset(&a, 0, sizeof(a));
     a.ix = *ix;
-    for (int j = 0; j < ix->d; ++j) {
-        double inv = 0.0;
-        if (is_pow2_width(ix->widths[j], &inv)) {
-            a.pow2 |= 1u << j;
-            a.inv_w[j] = inv;
-        }
-    }
+    a.pow2 = pow2_mask(ix, a.inv_w);
     a.Q = Q;
     a.q_dtype = q_dtype;
     a.nq = nq;
@@ -629,45 +689,14 @@ extern "C" int32_t ghn_query(const ghn_index_view *ix, const void *Q, int32_t q_
     a.mode = mode;
     a.task = task;
     a.out = *out;
-    a.qorder = nullptr;
-    if (ix->layout == GHN_LAYOUT_DENSE && nq >= BIN_MIN_QUERIES && workspace) {
+    a.qorder = qorder;
+    if (!qorder && ix->layout == GHN_LAYOUT_DENSE && nq >= BIN_MIN_QUERIES && workspace) {
         if (workspace_bytes < ghn_query_workspace_size(ix, nq)) {
             set_error("query workspace too small");
             return GHN_ERR_VALUE;
         }
-        char *ws = (char *)workspace;
-        BinConsts bc;
-        memset(&bc, 0, sizeof(bc));
-        for (int j = 0; j < ix->d; ++j) {
-            bc.w[j] = ix->widths[j];
-            bc.inv[j] = a.inv_w[j];
-            bc.lo[j] = ix->lo[j];
-            bc.ext[j] = ix->ext[j];
-        }
-        BinConsts *dbc = (BinConsts *)ws;
-        GHN_CUDA_CHECK(cudaMemcpyAsync(dbc, &bc, sizeof(bc), cudaMemcpyHostToDevice, s));
-        const size_t q4 = a256((size_t)nq * 4);
-        char *p = ws + a256(sizeof(BinConsts));
-        uint32_t *kin = (uint32_t *)p;
-        uint32_t *kout = (uint32_t *)(p + q4);
-        uint32_t *ktmp = (uint32_t *)(p + 2 * q4);
-        int32_t *vtmp = (int32_t *)(p + 3 * q4);
-        int32_t *order = (int32_t *)(p + 4 * q4);
-        char *rws = p + 5 * q4;
-        const int kb = bits_of((uint64_t)(ix->E > 0 ? ix->E - 1 : 0));
-        int keep = bits_of((uint64_t)nq) + 2;
-        if (keep > 24) keep = 24;
-        const int drop = kb > keep ? kb - keep : 0;
-        unsigned g = (unsigned)((nq + 255) / 256);
-        if (g > 148 * 16) g = 148 * 16;
-        if (q_dtype == GHN_F32)
-            query_bin_key_kernel<float><<<g, 256, 0, s>>>((const float *)Q, nq, ix->d, dbc->w, dbc->inv,
-                                                         a.pow2, dbc->lo, dbc->ext, drop, kin);
-        else
-            query_bin_key_kernel<double><<<g, 256, 0, s>>>((const double *)Q, nq, ix->d, dbc->w,
-                                                          dbc->inv, a.pow2, dbc->lo, dbc->ext, drop, kin);
-        GHN_LAUNCH_CHECK("query_bin_key_kernel");
-        int32_t rc = radix_sort_pairs(kin, nullptr, kout, order, ktmp, vtmp, nq, kb - drop, rws, s);
+        int32_t *order = (int32_t *)((char *)workspace + a256(sizeof(BinConsts)) + 4 * a256((size_t)nq * 4));
+        rc = ghn_query_order(ix, Q, q_dtype, nq, order, workspace, workspace_bytes, stream);
         if (rc) return rc;
         a.qorder = order;
     }

@@ -80,7 +80,7 @@ def _validate(index: GridIndex, Q, k: int, mode: str):
 
 
 def _run(index: GridIndex, Qt, k, mode, task, want_neighbors, want_stats, want_totals=False,
-         stream=None):
+         stream=None, qorder=None, want_confidence=True):
     import torch
 
     L = _lib.require_device()
@@ -104,19 +104,24 @@ def _run(index: GridIndex, Qt, k, mode, task, want_neighbors, want_stats, want_t
         if index._labels.codes is None:
             raise ValueError("labels are not classifiable")
         res["label"] = torch.empty(nq, dtype=torch.int32, device=dev)
-        res["confidence"] = torch.empty(nq, dtype=torch.float64, device=dev)
-        out.label, out.confidence = _lib.ptr(res["label"]), _lib.ptr(res["confidence"])
+        out.label = _lib.ptr(res["label"])
+        if want_confidence:
+            res["confidence"] = torch.empty(nq, dtype=torch.float64, device=dev)
+            out.confidence = _lib.ptr(res["confidence"])
     elif task == _lib.GHN_TASK_REGRESS_MEAN:
         if index._labels.targets is None:
             raise ValueError("labels are not numeric targets")
         res["value"] = torch.empty(nq, dtype=torch.float64, device=dev)
         out.value = _lib.ptr(res["value"])
     view = index.view()
-    wsz = int(L.ghn_query_workspace_size(ctypes.byref(view), nq))
-    ws = torch.empty(wsz, dtype=torch.uint8, device=dev)
+    if qorder is not None:
+        wsz, ws = 0, None
+    else:
+        wsz = int(L.ghn_query_workspace_size(ctypes.byref(view), nq))
+        ws = torch.empty(wsz, dtype=torch.uint8, device=dev)
     _lib.check(L.ghn_query(ctypes.byref(view), _lib.ptr(Qd), qdt, nq, k, _lib.GHN_MODE[mode], task,
-                           ctypes.byref(out), _lib.ptr(ws), wsz, _lib.stream_handle(stream)),
-               "ghn_query")
+                           _lib.ptr(qorder), ctypes.byref(out), _lib.ptr(ws), wsz,
+                           _lib.stream_handle(stream)), "ghn_query")
     res["_keepalive"] = (Qd, ws)
     return res
 
@@ -143,3 +148,23 @@ def knn_query(index: GridIndex, q, k: int, mode: str = "heuristic"):
     labels = index.labels
     nbrs = [Neighbor(float(dv), int(i), labels[int(i)]) for dv, i in zip(dist, idx)]
     return nbrs, QueryStats(int(st[0]), int(st[1]), int(st[2]))
+
+
+def query_order(index: GridIndex, Q, stream=None):
+    """K8 query binning: device int32 visit order sorted by central cell
+    (DENSE layout).  Results do not depend on the order; locality does."""
+    import torch
+
+    L = _lib.require_device()
+    Qd = torch.as_tensor(Q).to(index.X.device).contiguous()
+    if Qd.dtype not in (torch.float32, torch.float64):
+        Qd = Qd.to(torch.float64)
+    nq = int(Qd.shape[0])
+    qdt = _lib.GHN_F32 if Qd.dtype == torch.float32 else _lib.GHN_F64
+    view = index.view()
+    wsz = int(L.ghn_query_workspace_size(ctypes.byref(view), nq))
+    ws = torch.empty(wsz, dtype=torch.uint8, device=Qd.device)
+    order = torch.empty(nq, dtype=torch.int32, device=Qd.device)
+    _lib.check(L.ghn_query_order(ctypes.byref(view), _lib.ptr(Qd), qdt, nq, _lib.ptr(order),
+                                 _lib.ptr(ws), wsz, _lib.stream_handle(stream)), "ghn_query_order")
+    return order

@@ -59,19 +59,22 @@ TASKS = {"classify": _lib.GHN_TASK_CLASSIFY, "regress": _lib.GHN_TASK_REGRESS_ME
 
 
 def predict_batch(index: GridIndex, Q, k: int, mode: str = "heuristic", task: str = "classify",
-                  neighbors: bool = False, stats: bool = False, totals: bool = False, stream=None):
+                  neighbors: bool = False, stats: bool = False, totals: bool = False, stream=None,
+                  qorder=None, confidence: bool = True):
     """Fused device predict for nq queries (new API).
 
     Returns a dict of device tensors: task "classify" -> ``label`` (int32
     label codes; ``index.decode_labels`` maps them back) and ``confidence``;
     task "regress" -> ``value`` (fp64 mean).  Optional ``dist``/``idx``
     (neighbours), ``stats`` (nq, 3) and ``totals`` (sum layers, cells,
-    points, queries).
+    points, queries).  ``qorder``: a visit order from ``query_order`` (else
+    queries are binned internally).
     """
     if task not in TASKS:
         raise ValueError(f"unknown task {task!r}; expected one of {tuple(TASKS)}")
     Qt = _validate(index, Q, k, mode)
-    r = _run(index, Qt, k, mode, TASKS[task], neighbors, stats, want_totals=totals, stream=stream)
+    r = _run(index, Qt, k, mode, TASKS[task], neighbors, stats, want_totals=totals, stream=stream,
+             qorder=qorder, want_confidence=confidence)
     r.pop("_keepalive", None)
     return r
 
