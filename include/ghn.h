@@ -115,6 +115,7 @@ typedef struct ghn_index_view {
     const int32_t *ne_off;       /* DENSE */
     const int32_t *labels;       /* original point order; classify only */
     const double *targets;       /* original point order; regress only */
+    const int32_t *labels_perm;  /* labels in CSR slot order (ghn_gather_i32), or NULL */
 } ghn_index_view;
 
 typedef struct ghn_query_out {
@@ -127,8 +128,9 @@ typedef struct ghn_query_out {
     unsigned long long *totals;  /* [4] += sum layers, cells, points, queries, or NULL */
 } ghn_query_out;
 
-/* Workspace for query binning (sorting queries by their central cell). */
-size_t ghn_query_workspace_size(const ghn_index_view *ix, int64_t nq);
+/* Workspace for ghn_query / ghn_query_order with nq queries and this k
+ * (query binning, the tiled path's tile table and fallback list). */
+size_t ghn_query_workspace_size(const ghn_index_view *ix, int64_t nq, int32_t k);
 
 /* K8 query binning (new; the reference loops per query, bench.py:194):
  * order_out[t] = query visited t-th, sorted by central cell (DENSE layout;
@@ -144,6 +146,9 @@ int32_t ghn_query_order(const ghn_index_view *ix, const void *Q, int32_t q_dtype
 int32_t ghn_query(const ghn_index_view *ix, const void *Q, int32_t q_dtype, int64_t nq, int32_t k,
                   int32_t mode, int32_t task, const int32_t *qorder, const ghn_query_out *out,
                   void *workspace, size_t workspace_bytes, void *stream);
+
+/* dst[i] = src[idx[i]] for i < n (labels into CSR slot order). */
+int32_t ghn_gather_i32(const int32_t *src, const int32_t *idx, int64_t n, int32_t *dst, void *stream);
 
 /* Number of kernels this library has launched in this process (evidence for
  * the bench's gpu_launches; monotone, thread-safe). */

@@ -30,6 +30,7 @@ EXPORTS = (
     "ghn_query_workspace_size",
     "ghn_query_order",
     "ghn_query",
+    "ghn_gather_i32",
     "ghn_launch_count",
 )
 
@@ -63,7 +64,7 @@ class IndexView(ctypes.Structure):
         ("lo", _i64 * GHN_MAX_DIM),
         ("ext", _i64 * GHN_MAX_DIM),
         ("coords", _p), ("perm", _p), ("cell_start", _p), ("cell_ids", _p),
-        ("pt_off", _p), ("ne_off", _p), ("labels", _p), ("targets", _p),
+        ("pt_off", _p), ("ne_off", _p), ("labels", _p), ("targets", _p), ("labels_perm", _p),
     ]
 
 
@@ -98,7 +99,7 @@ def lib():
     L.ghn_fit_plan_init.restype = _i32
     L.ghn_fit_build.argtypes = [ctypes.POINTER(FitPlan), _p, ctypes.POINTER(FitOut), _p, _sz, _p]
     L.ghn_fit_build.restype = _i32
-    L.ghn_query_workspace_size.argtypes = [ctypes.POINTER(IndexView), _i64]
+    L.ghn_query_workspace_size.argtypes = [ctypes.POINTER(IndexView), _i64, _i32]
     L.ghn_query_workspace_size.restype = _sz
     L.ghn_query.argtypes = [ctypes.POINTER(IndexView), _p, _i32, _i64, _i32, _i32, _i32, _p,
                             ctypes.POINTER(QueryOut), _p, _sz, _p]
@@ -106,6 +107,8 @@ def lib():
     L.ghn_query_order.argtypes = [ctypes.POINTER(IndexView), _p, _i32, _i64, _p, _p, _sz, _p]
     L.ghn_query_order.restype = _i32
     L.ghn_launch_count.restype = ctypes.c_uint64
+    L.ghn_gather_i32.argtypes = [_p, _p, _i64, _p, _p]
+    L.ghn_gather_i32.restype = _i32
     _lib = L
     return L
 

@@ -22,6 +22,7 @@
 #include <string.h>
 
 #include "ghn_common.cuh"
+#include "ghn_tile2d.cuh"
 
 namespace ghn {
 namespace {
@@ -40,6 +41,7 @@ struct QArgs {
     int32_t mode;
     int32_t task;
     const int32_t *qorder;
+    const int32_t *nq_dev;   // device count (fallback list); overrides nq when set
     ghn_query_out out;
 };
 
@@ -337,11 +339,9 @@ __device__ double pairwise_mean(const double (&v)[KS], int k) {
 }
 
 template <typename T, int D, int KS>
-__global__ void __launch_bounds__(Q_THREADS) query_kernel(const QArgs a) {
+__device__ __forceinline__ void query_one(const QArgs &a, int64_t w) {
     constexpr int DM = D > 0 ? D : GHN_MAX_DIM;
     const int lane = lane_id();
-    const int64_t w = (int64_t)blockIdx.x * Q_WARPS + (threadIdx.x >> 5);
-    if (w >= a.nq) return;
     const int64_t qi = a.qorder ? (int64_t)a.qorder[w] : w;
     const ghn_index_view &ix = a.ix;
     const int d = D > 0 ? D : ix.d;
@@ -514,6 +514,14 @@ __global__ void __launch_bounds__(Q_THREADS) query_kernel(const QArgs a) {
     }
 }
 
+template <typename T, int D, int KS>
+__global__ void __launch_bounds__(Q_THREADS) query_kernel(const QArgs a) {
+    const int64_t nqv = a.nq_dev ? (int64_t)*a.nq_dev : a.nq;
+    for (int64_t w = (int64_t)blockIdx.x * Q_WARPS + (threadIdx.x >> 5); w < nqv;
+         w += (int64_t)gridDim.x * Q_WARPS)
+        query_one<T, D, KS>(a, w);
+}
+
 // ------------------------------------------------------------ query binning
 template <typename T>
 __global__ void query_bin_key_kernel(const T *__restrict__ Q, int64_t nq, int d, const double *w,
@@ -557,7 +565,9 @@ constexpr int64_t BIN_MIN_QUERIES = 2048;
 
 template <typename T, int D>
 int32_t launch_query_d(const QArgs &a, int ks, cudaStream_t s) {
-    const unsigned grid = (unsigned)((a.nq + Q_WARPS - 1) / Q_WARPS);
+    int64_t g = a.nq_dev ? 148LL * 8 : (a.nq + Q_WARPS - 1) / Q_WARPS;
+    if (g > 0x7fffffffLL) g = 0x7fffffffLL;
+    const unsigned grid = (unsigned)g;
     switch (ks) {
         case 1: query_kernel<T, D, 1><<<grid, Q_THREADS, 0, s>>>(a); break;
         case 2: query_kernel<T, D, 2><<<grid, Q_THREADS, 0, s>>>(a); break;
@@ -586,9 +596,19 @@ int32_t launch_query(const QArgs &a, int ks, cudaStream_t s) {
 
 using namespace ghn;
 
-extern "C" size_t ghn_query_workspace_size(const ghn_index_view *ix, int64_t nq) {
+static size_t order_workspace_bytes(int64_t nq) {
     size_t q4 = a256((size_t)(nq > 0 ? nq : 1) * 4);
     return a256(sizeof(BinConsts)) + 5 * q4 + a256(radix_workspace_bytes(nq > 0 ? nq : 1)) + 256;
+}
+
+extern "C" size_t ghn_query_workspace_size(const ghn_index_view *ix, int64_t nq, int32_t k) {
+    size_t b = order_workspace_bytes(nq);
+    Tile2dPlan tp;
+    if (tile2d_plan(ix, nq, k, GHN_TASK_CLASSIFY, false, &tp)) {
+        size_t t = tile2d_workspace_bytes(&tp, nq);
+        if (t > b) b = t;
+    }
+    return b;
 }
 
 static int32_t validate_query(const ghn_index_view *ix, int32_t k, int32_t mode) {
@@ -631,7 +651,7 @@ extern "C" int32_t ghn_query_order(const ghn_index_view *ix, const void *Q, int3
         return GHN_ERR_UNSUPPORTED;
     }
     if (nq <= 0) return GHN_OK;
-    if (!workspace || workspace_bytes < ghn_query_workspace_size(ix, nq)) {
+    if (!workspace || workspace_bytes < order_workspace_bytes(nq)) {
         set_error("query workspace too small");
         return GHN_ERR_VALUE;
     }
@@ -690,8 +710,23 @@ extern "C" int32_t ghn_query(const ghn_index_view *ix, const void *Q, int32_t q_
     a.task = task;
     a.out = *out;
     a.qorder = qorder;
+    a.nq_dev = nullptr;
+    const int ks = k <= 32 ? 1 : (k <= 64 ? 2 : (k <= 128 ? 4 : 8));
+    Tile2dPlan tp;
+    const bool want_nb = out->dist != nullptr || out->idx != nullptr;
+    if (workspace && tile2d_plan(ix, nq, k, task, want_nb, &tp) &&
+        workspace_bytes >= tile2d_workspace_bytes(&tp, nq)) {
+        int32_t *fb_list = nullptr, *fb_count = nullptr;
+        rc = tile2d_run(ix, &tp, Q, q_dtype, nq, k, mode, out, a.inv_w, a.pow2, workspace, &fb_list,
+                        &fb_count, s);
+        if (rc) return rc;
+        a.qorder = fb_list;
+        a.nq_dev = fb_count;
+        if (ix->dtype == GHN_F32) return launch_query<float>(a, ks, s);
+        return launch_query<double>(a, ks, s);
+    }
     if (!qorder && ix->layout == GHN_LAYOUT_DENSE && nq >= BIN_MIN_QUERIES && workspace) {
-        if (workspace_bytes < ghn_query_workspace_size(ix, nq)) {
+        if (workspace_bytes < order_workspace_bytes(nq)) {
             set_error("query workspace too small");
             return GHN_ERR_VALUE;
         }
@@ -700,7 +735,24 @@ extern "C" int32_t ghn_query(const ghn_index_view *ix, const void *Q, int32_t q_
         if (rc) return rc;
         a.qorder = order;
     }
-    const int ks = k <= 32 ? 1 : (k <= 64 ? 2 : (k <= 128 ? 4 : 8));
     if (ix->dtype == GHN_F32) return launch_query<float>(a, ks, s);
     return launch_query<double>(a, ks, s);
+}
+
+namespace ghn {
+__global__ void gather_i32_kernel(const int32_t *src, const int32_t *idx, int64_t n, int32_t *dst) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        dst[i] = src[idx[i]];
+}
+}  // namespace ghn
+
+extern "C" int32_t ghn_gather_i32(const int32_t *src, const int32_t *idx, int64_t n, int32_t *dst,
+                                  void *stream) {
+    if (n <= 0) return GHN_OK;
+    unsigned g = (unsigned)((n + 255) / 256);
+    if (g > 148 * 16) g = 148 * 16;
+    gather_i32_kernel<<<g, 256, 0, (cudaStream_t)stream>>>(src, idx, n, dst);
+    GHN_LAUNCH_CHECK("gather_i32_kernel");
+    return GHN_OK;
 }

@@ -1,0 +1,739 @@
+// ghn_tile2d.cu -- thread-per-query tiled predict for 2-D DENSE grids (sm_100a).
+//
+// The same results as query_kernel (explore.py:66-137 + predict.py:20-36),
+// organised for throughput:
+//   * queries are counting-sorted by a tile of T x T cells around their
+//     central cell (K8 binning); one CTA per tile stages the tile plus an
+//     apron of A layers -- coordinates (SoA fp32) and permuted labels -- in
+//     shared memory with coalesced row copies (one CSR row = one contiguous
+//     slot range);
+//   * one THREAD per query walks the Chebyshev shells over the staged cells;
+//   * the k-th (key, index) pair is found by a per-thread radix select over
+//     fp64 keys (32-bucket histograms on the monotone fp32 round-down of the
+//     key, re-bucketing until the boundary bucket holds <= 8 candidates,
+//     which are then ordered exactly) -- counting passes instead of a
+//     sorted insert per candidate;
+//   * the heuristic stop tests "some layer-l point precedes the current
+//     k-th" (equivalent to explore.py:117 `changed`), the guaranteed stop
+//     compares (l * min_w)^2 with the k-th key (explore.py:124-127);
+//   * the vote keeps per-label counts and the label's nearest member under
+//     (sqrt(key), index) (predict.py:29-35).
+// Queries whose centre is outside the grid, that need more than A layers,
+// whose tile overflows shared memory, whose boundary bucket cannot be split
+// (exact duplicate keys) or that meet more than T2_NL labels are appended to
+// a fallback list and answered by the generic warp-per-query kernel.
+#include <math.h>
+#include <stdio.h>
+#include <string.h>
+
+#include "ghn_common.cuh"
+#include "ghn_tile2d.cuh"
+
+namespace ghn {
+namespace {
+
+constexpr int T2_THREADS = 256;
+constexpr int T2_NB = 32;        // histogram buckets per select round
+constexpr int T2_SMALL = 4;      // boundary candidates ordered exactly
+constexpr int T2_NL = 4;         // distinct labels tracked by the vote
+constexpr int T2_CAP = 4096;     // staged points per tile
+
+struct T2Args {
+    int64_t n;
+    int32_t ext0, ext1;
+    int64_t lo0, lo1;
+    double w0, w1, inv0, inv1, min_w;
+    uint32_t pow2;
+    const float *c0;
+    const float *c1;
+    const int32_t *pt_off;
+    const int32_t *perm;
+    const int32_t *labels_perm;
+    const void *Q;
+    int32_t q_dtype;
+    int32_t k;
+    int32_t mode;
+    const int32_t *qorder;
+    const int32_t *tile_start;
+    int32_t T, A, nt0, nt1, win;
+    int32_t *out_label;
+    double *out_conf;
+    int64_t *out_stats;
+    unsigned long long *totals;
+    int32_t *fb_list;
+    int32_t *fb_count;
+};
+
+struct Win {
+    const float *sx;
+    const float *sy;
+    const int32_t *loc;     // (R, W+1) local slot of each cell start
+    const int32_t *delta;   // global slot = local + delta[row]
+    int R, W, W1;
+};
+
+// --------------------------------------------------------------- per warp
+// One warp answers one query at a time; lanes cover candidates.  A query's
+// candidate set is a short list of contiguous staged ranges (the rows of
+// the block around its cell, or the row segments / side cells of a shell),
+// held one range per lane and flattened by an inclusive scan.
+struct Ranges {
+    int s;      // this lane's range start (staged index)
+    int n;      // its length
+    int row;    // its window row (for the global slot)
+    int incl;   // inclusive prefix of lengths over lanes
+    int total;  // warp-uniform
+};
+
+__device__ __forceinline__ void ranges_finish(Ranges &rg) {
+    rg.incl = warp_inclusive_scan(rg.n);
+    rg.total = __shfl_sync(GHN_FULL, rg.incl, 31);
+}
+
+// Block(l): rows lr-l..lr+l, columns lc-l..lc+l (clipped), one row per lane.
+__device__ __forceinline__ Ranges block_ranges(const Win &w, int lr, int lc, int l) {
+    const int lane = lane_id();
+    Ranges rg{0, 0, 0, 0, 0};
+    const int i = lr - l + lane;
+    if (lane <= 2 * l && i >= 0 && i < w.R) {
+        const int a = max(lc - l, 0), b = min(lc + l, w.W - 1);
+        const int32_t *rp = w.loc + i * w.W1;
+        rg.s = rp[a];
+        rg.n = rp[b + 1] - rg.s;
+        rg.row = i;
+    }
+    ranges_finish(rg);
+    return rg;
+}
+
+// Shell(l), l >= 1: lanes 0/1 the full rows lr -+ l, lanes 2.. the side cells
+// lc -+ l of the rows in between (4l ranges, <= 32 for l <= 8).
+__device__ __forceinline__ Ranges shell_ranges(const Win &w, int lr, int lc, int l) {
+    const int lane = lane_id();
+    Ranges rg{0, 0, 0, 0, 0};
+    if (lane < 4 * l) {
+        int row, a, b;
+        if (lane < 2) {
+            row = lane == 0 ? lr - l : lr + l;
+            a = max(lc - l, 0);
+            b = min(lc + l, w.W - 1);
+        } else {
+            row = lr - l + 1 + ((lane - 2) >> 1);
+            a = b = ((lane - 2) & 1) ? lc + l : lc - l;
+        }
+        if (row >= 0 && row < w.R && a >= 0 && b < w.W && a <= b) {
+            const int32_t *rp = w.loc + row * w.W1;
+            rg.s = rp[a];
+            rg.n = rp[b + 1] - rg.s;
+            rg.row = row;
+        }
+    }
+    ranges_finish(rg);
+    return rg;
+}
+
+// Candidate m = base + lane of the flattened ranges -> staged index and row.
+__device__ __forceinline__ bool ranges_at(const Ranges &rg, int m, int &p, int &row) {
+    int L = 0;
+#pragma unroll
+    for (int step = 16; step >= 1; step >>= 1) {
+        const int v = __shfl_sync(GHN_FULL, rg.incl, L + step - 1);
+        if (v <= m) L += step;
+    }
+    L = L > 31 ? 31 : L;
+    const int exL = __shfl_sync(GHN_FULL, rg.incl - rg.n, L);
+    const int sL = __shfl_sync(GHN_FULL, rg.s, L);
+    row = __shfl_sync(GHN_FULL, rg.row, L);
+    p = sL + (m - exL);
+    return m < rg.total;
+}
+
+__device__ __forceinline__ double key2(const Win &w, int p, double q0, double q1) {
+    // numpy einsum order for d = 2: lane0 = d0^2, lane1 = d1^2, key = lane0 + lane1
+    const double d0 = __dsub_rn((double)w.sx[p], q0);
+    const double d1 = __dsub_rn((double)w.sy[p], q1);
+    return __dadd_rn(__dmul_rn(d0, d0), __dmul_rn(d1, d1));
+}
+
+struct Kth {
+    double key;
+    int32_t idx;
+};
+
+// Per-warp shared scratch.
+struct WarpScratch {
+    int hist[32];
+    double bkey[32];
+    int32_t bidx[32];
+    int32_t bg[32];
+};
+
+// Warp vote table: lane j holds label j's count (labels in first-met order).
+struct VoteW {
+    int32_t lab;    // this lane's label (valid for lane < used)
+    int32_t cnt;
+    int32_t used;   // warp-uniform
+    bool overflow;  // warp-uniform
+};
+
+// Add the member lanes (mask) with labels L to the table.
+__device__ __forceinline__ void vote_lanes(VoteW &v, unsigned members, int32_t L) {
+    const int lane = lane_id();
+    while (members) {
+        const int src = __ffs(members) - 1;
+        const int32_t lab = __shfl_sync(GHN_FULL, L, src);
+        const unsigned same = __ballot_sync(GHN_FULL, ((members >> lane) & 1u) && L == lab);
+        members &= ~same;
+        const int c = __popc(same);
+        const unsigned hit = __ballot_sync(GHN_FULL, lane < v.used && v.lab == lab);
+        if (hit) {
+            if (lane == __ffs(hit) - 1) v.cnt += c;
+        } else if (v.used < 32) {
+            if (lane == v.used) {
+                v.lab = lab;
+                v.cnt = c;
+            }
+            ++v.used;
+        } else {
+            v.overflow = true;
+        }
+    }
+}
+
+__device__ __forceinline__ bool lt_pair(double ka, int32_t ia, double kb, int32_t ib) {
+    return ka < kb || (ka == kb && ia < ib);
+}
+
+// Radix select over the candidates of `rg` with key in [lo, hi]: the r-th
+// smallest (key, index) and the vote over the r members.  Level-1 buckets on
+// the monotone fp32 round-down of the key (32 buckets, one per lane), a
+// level-2 split of the boundary bucket when it holds more than 32, then the
+// boundary candidates are ranked exactly.  False = cannot resolve.
+__device__ __forceinline__ bool select_vote_w(const T2Args &a, const Win &w, WarpScratch &sc,
+                                              const Ranges &rg, double q0, double q1, int r,
+                                              double lo, double hi, Kth &out, VoteW &v) {
+    const int lane = lane_id();
+    const float flo = __double2float_rd(lo);
+    const float fhi = __double2float_ru(hi);
+    const float sc1 = fhi > flo ? fminf(32.0f * __frcp_rn(fhi - flo), 1e30f) : 0.0f;
+#define T2_B1(k32) min((int)(((k32) - flo) * sc1), 31)
+    sc.hist[lane] = 0;
+    __syncwarp();
+    for (int base = 0; base < rg.total; base += 32) {
+        int p, row;
+        const bool act = ranges_at(rg, base + lane, p, row);
+        double key = 0.0;
+        if (act) key = key2(w, p, q0, q1);
+        const bool in = act && key >= lo && key <= hi;
+        const int b = in ? T2_B1(__double2float_rd(key)) : -1;
+        const unsigned im = __ballot_sync(GHN_FULL, in);
+        if (in) {
+            const unsigned grp = __match_any_sync(im, b);
+            if ((grp & lanemask_lt()) == 0) atomicAdd(&sc.hist[b], __popc(grp));
+        }
+    }
+    __syncwarp();
+    int c = sc.hist[lane];
+    int incl = warp_inclusive_scan(c);
+    unsigned ge = __ballot_sync(GHN_FULL, incl >= r);
+    if (!ge) return false;
+    const int bs1 = __ffs(ge) - 1;
+    int m = __shfl_sync(GHN_FULL, c, bs1);
+    r -= __shfl_sync(GHN_FULL, incl - c, bs1);
+    int bs2 = -1;
+    float lo2 = 0.0f, sc2 = 0.0f;
+    if (m > 32) {
+        lo2 = flo + (float)bs1 / sc1;
+        sc2 = fminf(sc1 * 32.0f, 1e30f);
+#define T2_B2(k32) max(0, min((int)(((k32) - lo2) * sc2), 31))
+        __syncwarp();
+        sc.hist[lane] = 0;
+        __syncwarp();
+        for (int base = 0; base < rg.total; base += 32) {
+            int p, row;
+            const bool act = ranges_at(rg, base + lane, p, row);
+            double key = 0.0;
+            if (act) key = key2(w, p, q0, q1);
+            bool in = act && key >= lo && key <= hi;
+            int b = -1;
+            if (in) {
+                const float k32 = __double2float_rd(key);
+                in = T2_B1(k32) == bs1;
+                b = T2_B2(k32);
+            }
+            const unsigned im = __ballot_sync(GHN_FULL, in);
+            if (in) {
+                const unsigned grp = __match_any_sync(im, b);
+                if ((grp & lanemask_lt()) == 0) atomicAdd(&sc.hist[b], __popc(grp));
+            }
+        }
+        __syncwarp();
+        c = sc.hist[lane];
+        incl = warp_inclusive_scan(c);
+        ge = __ballot_sync(GHN_FULL, incl >= r);
+        if (!ge) return false;
+        bs2 = __ffs(ge) - 1;
+        m = __shfl_sync(GHN_FULL, c, bs2);
+        r -= __shfl_sync(GHN_FULL, incl - c, bs2);
+        if (m > 32) return false;
+    }
+    // collect: members below the boundary vote now; boundary candidates are
+    // compacted into the scratch and ranked exactly afterwards
+    v.lab = 0;
+    v.cnt = 0;
+    v.used = 0;
+    v.overflow = false;
+    int nb = 0;
+    for (int base = 0; base < rg.total; base += 32) {
+        int p, row;
+        const bool act = ranges_at(rg, base + lane, p, row);
+        double key = 0.0;
+        if (act) key = key2(w, p, q0, q1);
+        int side = 1;
+        if (act && key >= lo && key <= hi) {
+            const float k32 = __double2float_rd(key);
+            const int b1 = T2_B1(k32);
+            side = b1 < bs1 ? -1 : (b1 > bs1 ? 1 : 0);
+            if (side == 0 && bs2 >= 0) {
+                const int b2 = T2_B2(k32);
+                side = b2 < bs2 ? -1 : (b2 > bs2 ? 1 : 0);
+            }
+        }
+        const int32_t g = p + w.delta[row];
+        const unsigned mem = __ballot_sync(GHN_FULL, side < 0);
+        if (mem) {
+            const int32_t L = side < 0 ? a.labels_perm[g] : 0;
+            vote_lanes(v, mem, L);
+        }
+        const unsigned bnd = __ballot_sync(GHN_FULL, side == 0);
+        if (side == 0) {
+            const int pos = nb + __popc(bnd & lanemask_lt());
+            sc.bkey[pos] = key;
+            sc.bidx[pos] = a.perm[g];
+            sc.bg[pos] = g;
+        }
+        nb += __popc(bnd);
+    }
+#undef T2_B1
+#undef T2_B2
+    __syncwarp();
+    // rank the nb (== m) boundary candidates exactly
+    double mk = INFINITY;
+    int32_t mi = 0x7fffffff, mg = 0;
+    if (lane < nb) {
+        mk = sc.bkey[lane];
+        mi = sc.bidx[lane];
+        mg = sc.bg[lane];
+    }
+    int rank = 0;
+    for (int t = 0; t < nb; ++t) {
+        const double tk = __shfl_sync(GHN_FULL, mk, t);
+        const int32_t ti = __shfl_sync(GHN_FULL, mi, t);
+        rank += lt_pair(tk, ti, mk, mi) ? 1 : 0;
+    }
+    const bool memb = lane < nb && rank < r;
+    const unsigned bm = __ballot_sync(GHN_FULL, memb);
+    if (bm) vote_lanes(v, bm, memb ? a.labels_perm[mg] : 0);
+    const unsigned kl = __ballot_sync(GHN_FULL, lane < nb && rank == r - 1);
+    if (!kl) return false;
+    const int src = __ffs(kl) - 1;
+    out.key = __shfl_sync(GHN_FULL, mk, src);
+    out.idx = __shfl_sync(GHN_FULL, mi, src);
+    __syncwarp();
+    return !v.overflow;
+}
+
+// Tie-break among the labels tied at the top count: the label of the member
+// minimising (sqrt(key), index) (predict.py:30-35), over the k members.
+__device__ __forceinline__ int32_t vote_tiebreak(const T2Args &a, const Win &w, const Ranges &rg,
+                                                 double q0, double q1, const Kth &kth, const VoteW &v,
+                                                 int top) {
+    const int lane = lane_id();
+    double bd = INFINITY, bkey = INFINITY;
+    int32_t bi = 0x7fffffff, bl = 0;
+    for (int base = 0; base < rg.total; base += 32) {
+        int p, row;
+        const bool act = ranges_at(rg, base + lane, p, row);
+        double key = INFINITY;
+        int32_t idx = 0x7fffffff, L = 0;
+        bool member = false;
+        if (act) {
+            key = key2(w, p, q0, q1);
+            const int32_t g = p + w.delta[row];
+            if (key <= kth.key) {
+                idx = a.perm[g];
+                member = key < kth.key || idx <= kth.idx;
+                if (member) L = a.labels_perm[g];
+            }
+        }
+        bool tied = false;
+        for (int t = 0; t < v.used; ++t) {
+            const int32_t tl = __shfl_sync(GHN_FULL, v.lab, t);
+            const int32_t tc = __shfl_sync(GHN_FULL, v.cnt, t);
+            tied |= member && tl == L && tc == top;
+        }
+        if (tied) {
+            const double dd = sqrt(key);
+            if (dd < bd || (dd == bd && idx < bi)) {
+                bd = dd;
+                bi = idx;
+                bl = L;
+                bkey = key;
+            }
+        }
+    }
+    (void)bkey;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        const double od = __shfl_xor_sync(GHN_FULL, bd, off);
+        const int32_t oi = __shfl_xor_sync(GHN_FULL, bi, off);
+        const int32_t ol = __shfl_xor_sync(GHN_FULL, bl, off);
+        if (od < bd || (od == bd && oi < bi)) {
+            bd = od;
+            bi = oi;
+            bl = ol;
+        }
+    }
+    return bl;
+}
+
+__device__ __forceinline__ void push_fallback(const T2Args &a, int32_t qi) {
+    const int32_t slot = atomicAdd(a.fb_count, 1);
+    a.fb_list[slot] = qi;
+}
+
+// Non-empty cells of block(l) (QueryStats; only when stats are requested).
+__device__ __forceinline__ int block_cells(const Win &w, int lr, int lc, int l) {
+    const int lane = lane_id();
+    const int side = 2 * l + 1;
+    int cells = 0;
+    for (int e = lane; e < side * side; e += 32) {
+        const int i = lr - l + e / side, j = lc - l + e % side;
+        if (i >= 0 && i < w.R && j >= 0 && j < w.W) {
+            const int32_t *rp = w.loc + i * w.W1;
+            cells += rp[j + 1] > rp[j];
+        }
+    }
+    return warp_sum(cells);
+}
+
+__device__ __forceinline__ void process_query_w(const T2Args &a, const Win &w, WarpScratch &sc, int qq,
+                                                int t0, int t1, int r_lo, int c_lo, bool want_stats) {
+    const int lane = lane_id();
+    const int32_t qi = a.qorder[qq];
+    double q0, q1;
+    if (a.q_dtype == GHN_F32) {
+        q0 = (double)((const float *)a.Q)[2 * (int64_t)qi];
+        q1 = (double)((const float *)a.Q)[2 * (int64_t)qi + 1];
+    } else {
+        q0 = ((const double *)a.Q)[2 * (int64_t)qi];
+        q1 = ((const double *)a.Q)[2 * (int64_t)qi + 1];
+    }
+    const int64_t cc0 = cell_id(q0, a.w0, a.inv0, a.pow2 & 1u) - a.lo0;
+    const int64_t cc1 = cell_id(q1, a.w1, a.inv1, (a.pow2 >> 1) & 1u) - a.lo1;
+    const int64_t tr0 = (int64_t)t0 * a.T, tc0 = (int64_t)t1 * a.T;
+    if (cc0 < tr0 || cc0 >= tr0 + a.T || cc1 < tc0 || cc1 >= tc0 + a.T || cc0 >= a.ext0 ||
+        cc1 >= a.ext1) {
+        if (lane == 0) push_fallback(a, qi);   // centre outside the grid
+        return;
+    }
+    const int lr = (int)(cc0 - r_lo), lc = (int)(cc1 - c_lo);
+    const int lmax = max(max((int)cc0, a.ext0 - 1 - (int)cc0), max((int)cc1, a.ext1 - 1 - (int)cc1));
+    const int k = a.k;
+    // phase 1: whole layers enter while fewer than k points are buffered
+    int l = 0;
+    Ranges blk;
+    for (;; ++l) {
+        if (l > a.A) {
+            if (lane == 0) push_fallback(a, qi);
+            return;
+        }
+        blk = block_ranges(w, lr, lc, l);
+        if (blk.total >= k || l >= lmax) break;
+    }
+    int64_t points = blk.total;
+    int64_t cells = want_stats ? block_cells(w, lr, lc, l) : 0;
+    int layers = l;
+    Kth kth{INFINITY, 0x7fffffff};
+    VoteW v{0, 0, 0, false};
+    {
+        const double e0 = fmax(q0 - (double)(a.lo0 + cc0 - l) * a.w0, (double)(a.lo0 + cc0 + l + 1) * a.w0 - q0);
+        const double e1 = fmax(q1 - (double)(a.lo1 + cc1 - l) * a.w1, (double)(a.lo1 + cc1 + l + 1) * a.w1 - q1);
+        const double hi = (e0 * e0 + e1 * e1) * (1.0 + 1e-6) + 1e-300;
+        if (blk.total < k || !select_vote_w(a, w, sc, blk, q0, q1, k, 0.0, hi, kth, v)) {
+            if (lane == 0) push_fallback(a, qi);
+            return;
+        }
+    }
+    // the layer that filled the buffer `changed`; the guaranteed bound may stop
+    bool stop = false;
+    if (a.mode == GHN_MODE_GUARANTEED) {
+        const double b = __dmul_rn((double)l, a.min_w);
+        if (__dmul_rn(b, b) > kth.key) stop = true;
+    }
+    // phase 2: a later layer matters only if one of its points precedes the k-th
+    while (!stop && l < lmax) {
+        ++l;
+        if (l > a.A) {
+            if (lane == 0) push_fallback(a, qi);
+            return;
+        }
+        const Ranges sh = shell_ranges(w, lr, lc, l);
+        int below = 0;
+        for (int base = 0; base < sh.total; base += 32) {
+            int p, row;
+            const bool act = ranges_at(sh, base + lane, p, row);
+            bool lt = false;
+            if (act) {
+                const double key = key2(w, p, q0, q1);
+                lt = key < kth.key || (key == kth.key && a.perm[p + w.delta[row]] < kth.idx);
+            }
+            below += __popc(__ballot_sync(GHN_FULL, lt));
+        }
+        points += sh.total;
+        layers = l;
+        if (want_stats) cells = block_cells(w, lr, lc, l);
+        const bool changed = below > 0;
+        if (changed) {
+            blk = block_ranges(w, lr, lc, l);
+            if (!select_vote_w(a, w, sc, blk, q0, q1, k, 0.0, kth.key, kth, v)) {
+                if (lane == 0) push_fallback(a, qi);
+                return;
+            }
+        }
+        if (a.mode == GHN_MODE_HEURISTIC && !changed) stop = true;
+        if (a.mode == GHN_MODE_GUARANTEED) {
+            const double b = __dmul_rn((double)l, a.min_w);
+            if (__dmul_rn(b, b) > kth.key) stop = true;
+        }
+    }
+    // winner: top count; ties -> nearest member by (sqrt(key), index)
+    const int top = warp_max(lane < v.used ? v.cnt : 0);
+    const unsigned tiedm = __ballot_sync(GHN_FULL, lane < v.used && v.cnt == top);
+    int32_t wl = __shfl_sync(GHN_FULL, v.lab, __ffs(tiedm) - 1);
+    if (__popc(tiedm) > 1) {
+        // members are the candidates of the last selected block
+        wl = vote_tiebreak(a, w, blk, q0, q1, kth, v, top);
+    }
+    if (lane == 0) {
+        if (a.out_label) a.out_label[qi] = wl;
+        if (a.out_conf) a.out_conf[qi] = __ddiv_rn((double)top, (double)k);
+        if (a.out_stats) {
+            a.out_stats[3 * (int64_t)qi + 0] = layers;
+            a.out_stats[3 * (int64_t)qi + 1] = cells;
+            a.out_stats[3 * (int64_t)qi + 2] = points;
+        }
+        if (a.totals) {
+            atomicAdd(&a.totals[0], (unsigned long long)layers);
+            atomicAdd(&a.totals[1], (unsigned long long)cells);
+            atomicAdd(&a.totals[2], (unsigned long long)points);
+            atomicAdd(&a.totals[3], 1ull);
+        }
+    }
+}
+
+__global__ void __launch_bounds__(T2_THREADS) tile2d_kernel(const T2Args a) {
+    extern __shared__ __align__(16) unsigned char sm[];
+    __shared__ int s_P;
+    __shared__ WarpScratch s_scratch[T2_THREADS / 32];
+    const int t = blockIdx.x;
+    const int qb = a.tile_start[t], qe = a.tile_start[t + 1];
+    if (qb == qe) return;
+    const int t0 = t / a.nt1, t1 = t - (t / a.nt1) * a.nt1;
+    const int r_lo = max(t0 * a.T - a.A, 0), r_hi = min(t0 * a.T + a.T - 1 + a.A, a.ext0 - 1);
+    const int c_lo = max(t1 * a.T - a.A, 0), c_hi = min(t1 * a.T + a.T - 1 + a.A, a.ext1 - 1);
+    const int R = r_hi - r_lo + 1, W = c_hi - c_lo + 1, W1 = W + 1;
+    float *sx = (float *)sm;
+    float *sy = sx + T2_CAP;
+    int32_t *loc = (int32_t *)(sy + T2_CAP);                       // [R][W+1]
+    int32_t *delta = loc + a.win * (a.win + 1);                    // [R]
+    int32_t *rstart = delta + a.win;                               // [R+1]
+    for (int e = threadIdx.x; e < R * W1; e += blockDim.x) {
+        const int i = e / W1, j = e - (e / W1) * W1;
+        loc[e] = a.pt_off[(int64_t)(r_lo + i) * a.ext1 + c_lo + j];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int s = 0;
+        for (int i = 0; i < R; ++i) {
+            rstart[i] = s;
+            delta[i] = loc[i * W1] - s;
+            s += loc[i * W1 + W] - loc[i * W1];
+        }
+        rstart[R] = s;
+        s_P = s;
+    }
+    __syncthreads();
+    const int P = s_P;
+    if (P > T2_CAP) {
+        for (int qq = qb + threadIdx.x; qq < qe; qq += blockDim.x) push_fallback(a, a.qorder[qq]);
+        return;
+    }
+    for (int e = threadIdx.x; e < R * W1; e += blockDim.x) loc[e] -= delta[e / W1];
+    for (int p = threadIdx.x; p < P; p += blockDim.x) {
+        int lo = 0, hi = R - 1;
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (rstart[mid] <= p) lo = mid;
+            else hi = mid - 1;
+        }
+        const int32_t g = p + delta[lo];
+        sx[p] = a.c0[g];
+        sy[p] = a.c1[g];
+    }
+    __syncthreads();
+    Win w{sx, sy, loc, delta, R, W, W1};
+    const int warp = threadIdx.x >> 5;
+    const bool want_stats = a.out_stats != nullptr || a.totals != nullptr;
+    for (int qq = qb + warp; qq < qe; qq += T2_THREADS / 32)
+        process_query_w(a, w, s_scratch[warp], qq, t0, t1, r_lo, c_lo, want_stats);
+}
+
+// ------------------------------------------------------------------ binning
+__global__ void tile_key_kernel(const void *Q, int32_t q_dtype, int64_t nq, double w0, double w1,
+                                double inv0, double inv1, uint32_t pow2, int64_t lo0, int64_t lo1,
+                                int32_t ext0, int32_t ext1, int32_t T, int32_t nt1, int32_t *keys,
+                                int32_t *counts) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nq;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        double q0, q1;
+        if (q_dtype == GHN_F32) {
+            q0 = ((const float *)Q)[2 * i];
+            q1 = ((const float *)Q)[2 * i + 1];
+        } else {
+            q0 = ((const double *)Q)[2 * i];
+            q1 = ((const double *)Q)[2 * i + 1];
+        }
+        int64_t c0 = cell_id(q0, w0, inv0, pow2 & 1u) - lo0;
+        int64_t c1 = cell_id(q1, w1, inv1, (pow2 >> 1) & 1u) - lo1;
+        c0 = c0 < 0 ? 0 : (c0 >= ext0 ? ext0 - 1 : c0);
+        c1 = c1 < 0 ? 0 : (c1 >= ext1 ? ext1 - 1 : c1);
+        const int32_t key = (int32_t)(c0 / T) * nt1 + (int32_t)(c1 / T);
+        keys[i] = key;
+        atomicAdd(&counts[key], 1);
+    }
+}
+
+__global__ void tile_scatter_kernel(const int32_t *keys, int64_t nq, const int32_t *tile_start,
+                                    int32_t *cursor, int32_t *order) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nq;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t key = keys[i];
+        order[tile_start[key] + atomicAdd(&cursor[key], 1)] = (int32_t)i;
+    }
+}
+
+size_t a256(size_t b) { return (b + 255) & ~(size_t)255; }
+
+}  // namespace
+
+bool tile2d_plan(const ghn_index_view *ix, int64_t nq, int32_t k, int32_t task, bool want_neighbors,
+                 Tile2dPlan *plan) {
+    memset(plan, 0, sizeof(*plan));
+    if (ix->layout != GHN_LAYOUT_DENSE || ix->d != 2 || ix->dtype != GHN_F32) return false;
+    if (task != GHN_TASK_CLASSIFY || want_neighbors || !ix->labels_perm) return false;
+    if (nq < 4096 || k < 1 || k > 256) return false;
+    const double rho = (double)ix->n / (double)ix->E;      // points per bbox cell
+    int lf = 0;
+    while (lf < 8 && (2.0 * lf + 1) * (2.0 * lf + 1) * rho < (double)k) ++lf;
+    const int A = lf + 2 > 4 ? 4 : lf + 2;
+    int T = (int)floor(sqrt(0.7 * T2_CAP / (rho > 1e-9 ? rho : 1e-9))) - 2 * A;
+    const double Tmax = sqrt((double)ix->E / (148.0 * 4.0));
+    if (T > Tmax) T = (int)Tmax;
+    if (T > 64) T = 64;
+    if (T < 1) return false;
+    plan->T = T;
+    plan->A = A;
+    plan->nt0 = (int32_t)((ix->ext[0] + T - 1) / T);
+    plan->nt1 = (int32_t)((ix->ext[1] + T - 1) / T);
+    plan->ntiles = (int64_t)plan->nt0 * plan->nt1;
+    plan->win = T + 2 * A;
+    plan->smem = (size_t)T2_CAP * 8 +
+                 (size_t)plan->win * (plan->win + 1) * 4 + (size_t)plan->win * 4 +
+                 (size_t)(plan->win + 1) * 4 + 64;
+    if (plan->smem > 200 * 1024) return false;
+    return true;
+}
+
+size_t tile2d_workspace_bytes(const Tile2dPlan *p, int64_t nq) {
+    const size_t q4 = a256((size_t)nq * 4);
+    const size_t t4 = a256((size_t)(p->ntiles + 1) * 4);
+    return 3 * q4 + 3 * t4 + scan_workspace_bytes(p->ntiles + 1) + 256;
+}
+
+int32_t tile2d_run(const ghn_index_view *ix, const Tile2dPlan *plan, const void *Q, int32_t q_dtype,
+                   int64_t nq, int32_t k, int32_t mode, const ghn_query_out *out, const double *inv_w,
+                   uint32_t pow2, void *workspace, int32_t **fb_list, int32_t **fb_count,
+                   cudaStream_t s) {
+    char *ws = (char *)workspace;
+    const size_t q4 = a256((size_t)nq * 4);
+    const size_t t4 = a256((size_t)(plan->ntiles + 1) * 4);
+    int32_t *keys = (int32_t *)ws;
+    int32_t *order = (int32_t *)(ws + q4);
+    int32_t *fbl = (int32_t *)(ws + 2 * q4);
+    int32_t *tstart = (int32_t *)(ws + 3 * q4);
+    int32_t *cursor = (int32_t *)(ws + 3 * q4 + t4);
+    int32_t *fbc = (int32_t *)(ws + 3 * q4 + 2 * t4);
+    char *sws = ws + 3 * q4 + 3 * t4;
+    GHN_CUDA_CHECK(cudaMemsetAsync(tstart, 0, (size_t)(plan->ntiles + 1) * 4, s));
+    GHN_CUDA_CHECK(cudaMemsetAsync(cursor, 0, (size_t)(plan->ntiles + 1) * 4, s));
+    GHN_CUDA_CHECK(cudaMemsetAsync(fbc, 0, 4, s));
+    unsigned g = (unsigned)((nq + 255) / 256);
+    if (g > 148 * 16) g = 148 * 16;
+    tile_key_kernel<<<g, 256, 0, s>>>(Q, q_dtype, nq, ix->widths[0], ix->widths[1], inv_w[0], inv_w[1],
+                                      pow2, ix->lo[0], ix->lo[1], (int32_t)ix->ext[0],
+                                      (int32_t)ix->ext[1], plan->T, plan->nt1, keys, tstart);
+    GHN_LAUNCH_CHECK("tile_key_kernel");
+    int32_t rc = exclusive_scan_i32(tstart, tstart, plan->ntiles + 1, sws, s);
+    if (rc) return rc;
+    tile_scatter_kernel<<<g, 256, 0, s>>>(keys, nq, tstart, cursor, order);
+    GHN_LAUNCH_CHECK("tile_scatter_kernel");
+    T2Args a;
+    memset(&a, 0, sizeof(a));
+    a.n = ix->n;
+    a.ext0 = (int32_t)ix->ext[0];
+    a.ext1 = (int32_t)ix->ext[1];
+    a.lo0 = ix->lo[0];
+    a.lo1 = ix->lo[1];
+    a.w0 = ix->widths[0];
+    a.w1 = ix->widths[1];
+    a.inv0 = inv_w[0];
+    a.inv1 = inv_w[1];
+    a.pow2 = pow2;
+    a.min_w = ix->min_width;
+    a.c0 = (const float *)ix->coords;
+    a.c1 = (const float *)ix->coords + ix->n;
+    a.pt_off = ix->pt_off;
+    a.perm = ix->perm;
+    a.labels_perm = ix->labels_perm;
+    a.Q = Q;
+    a.q_dtype = q_dtype;
+    a.k = k;
+    a.mode = mode;
+    a.qorder = order;
+    a.tile_start = tstart;
+    a.T = plan->T;
+    a.A = plan->A;
+    a.nt0 = plan->nt0;
+    a.nt1 = plan->nt1;
+    a.win = plan->win;
+    a.out_label = out->label;
+    a.out_conf = out->confidence;
+    a.out_stats = out->stats;
+    a.totals = out->totals;
+    a.fb_list = fbl;
+    a.fb_count = fbc;
+    static bool attr_set = false;
+    if (!attr_set) {
+        GHN_CUDA_CHECK(cudaFuncSetAttribute(tile2d_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            200 * 1024));
+        attr_set = true;
+    }
+    tile2d_kernel<<<(unsigned)plan->ntiles, T2_THREADS, plan->smem, s>>>(a);
+    GHN_LAUNCH_CHECK("tile2d_kernel");
+    *fb_list = fbl;
+    *fb_count = fbc;
+    return GHN_OK;
+}
+
+}  // namespace ghn

@@ -117,7 +117,7 @@ def _run(index: GridIndex, Qt, k, mode, task, want_neighbors, want_stats, want_t
     if qorder is not None:
         wsz, ws = 0, None
     else:
-        wsz = int(L.ghn_query_workspace_size(ctypes.byref(view), nq))
+        wsz = int(L.ghn_query_workspace_size(ctypes.byref(view), nq, k))
         ws = torch.empty(wsz, dtype=torch.uint8, device=dev)
     _lib.check(L.ghn_query(ctypes.byref(view), _lib.ptr(Qd), qdt, nq, k, _lib.GHN_MODE[mode], task,
                            _lib.ptr(qorder), ctypes.byref(out), _lib.ptr(ws), wsz,
@@ -162,7 +162,7 @@ def query_order(index: GridIndex, Q, stream=None):
     nq = int(Qd.shape[0])
     qdt = _lib.GHN_F32 if Qd.dtype == torch.float32 else _lib.GHN_F64
     view = index.view()
-    wsz = int(L.ghn_query_workspace_size(ctypes.byref(view), nq))
+    wsz = int(L.ghn_query_workspace_size(ctypes.byref(view), nq, 1))
     ws = torch.empty(wsz, dtype=torch.uint8, device=Qd.device)
     order = torch.empty(nq, dtype=torch.int32, device=Qd.device)
     _lib.check(L.ghn_query_order(ctypes.byref(view), _lib.ptr(Qd), qdt, nq, _lib.ptr(order),

@@ -132,6 +132,7 @@ class GridIndex:
         self.cell_ids = t["cell_ids"]
         self.pt_off = t.get("pt_off")
         self.ne_off = t.get("ne_off")
+        self.labels_perm = t.get("labels_perm")
         self.n_cells = int(n_cells)
         self.lo = np.array(plan.lo[: plan.d], dtype=np.int64)
         self.ext = np.array(plan.ext[: plan.d], dtype=np.int64)
@@ -221,6 +222,7 @@ class GridIndex:
         v.ne_off = _lib.ptr(self.ne_off)
         v.labels = _lib.ptr(self._labels.codes)
         v.targets = _lib.ptr(self._labels.targets)
+        v.labels_perm = _lib.ptr(self.labels_perm)
         return v
 
 
@@ -338,6 +340,10 @@ def build_arrays(X, y=None, params: GridParams | None = None, cells_per_axis=Non
     n_cells = int(t["n_cells"].item())
     del ws
     labels = _Labels(y if y is not None else [0] * n, dev)
+    if labels.codes is not None:
+        t["labels_perm"] = torch.empty(n, dtype=i32, device=dev)
+        _lib.check(L.ghn_gather_i32(_lib.ptr(labels.codes), _lib.ptr(t["perm"]), n,
+                                    _lib.ptr(t["labels_perm"]), s), "ghn_gather_i32")
     return GridIndex(params, metric, Xd, labels, plan, t, n_cells)
 
 

@@ -1,0 +1,109 @@
+"""GPU parity on BASELINE.json-shaped workloads against the C oracle.
+
+Bit-exact: bucket order, neighbour indices, distances, QueryStats, vote
+labels and confidences, regression means.  Covers both predict kernels:
+the tiled thread-per-query kernel (2-D dense, classify) and the generic
+warp-per-query kernel (everything else, and the tiled kernel's fallbacks).
+"""
+import numpy as np
+import pytest
+
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ghn():
+    import paper_2004_02290_b200 as g
+
+    return g
+
+
+def _check_predict(ghn, index, ref, X, y, Q, k, mode, task="classify"):
+    r = ghn.predict_batch(index, Q, k, mode, task=task, stats=True)
+    keys, idx, stats = ref.query(Q, k, mode)
+    assert np.array_equal(r["stats"].cpu().numpy(), stats), "QueryStats"
+    if task == "classify":
+        lab, conf = oracle.classify(keys, idx, np.asarray(y, dtype=np.int64))
+        got = r["label"].cpu().numpy().astype(np.int64)
+        bad = np.flatnonzero(got != lab)
+        assert bad.size == 0, f"{bad.size} label mismatches, first {bad[:5]}"
+        assert np.array_equal(r["confidence"].cpu().numpy(), conf)
+    else:
+        val = oracle.regress_mean(idx, np.asarray(y, dtype=np.float64))
+        assert np.array_equal(r["value"].cpu().numpy(), val)
+    return keys, idx, stats
+
+
+def _check_knn(ghn, index, ref, Q, k, mode):
+    dist, idx, stats = ghn.knn_query_batch(index, Q, k, mode)
+    keys, ridx, rstats = ref.query(Q, k, mode)
+    assert np.array_equal(idx.cpu().numpy(), ridx)
+    assert np.array_equal(dist.cpu().numpy(), np.sqrt(keys))
+    assert np.array_equal(stats.cpu().numpy(), rstats)
+
+
+@pytest.mark.parametrize("mode", ["heuristic", "guaranteed"])
+def test_cfg0_full(ghn, mode):
+    from paper_2004_02290_b200 import datagen
+
+    w = datagen.cfg0()
+    index = ghn.build_arrays(w.X, w.y, cells_per_axis=w.cells_per_axis)
+    ref = oracle.COracle(w.X, w.widths)
+    order, _, starts, _, _ = ref.export()
+    assert np.array_equal(index.order, order)
+    assert np.array_equal(index.bucket_starts, starts)
+    _check_predict(ghn, index, ref, w.X, w.y, w.Q, w.k, mode)
+    _check_knn(ghn, index, ref, w.Q, w.k, mode)
+
+
+@pytest.mark.parametrize("k", [1, 4, 16, 64])
+def test_cfg4_shaped_non_pow2_width(ghn, k):
+    """cfg4 recipe at 4M points on an 820 x 820 grid (width 1/820 is not a power
+    of two, so cell ids take the fp64-division path), 100k queries, plus
+    outlier queries that must fall back to the generic kernel."""
+    from paper_2004_02290_b200 import datagen
+
+    w = datagen.cfg4(n=4_000_000, nq=100_000, seed=41)
+    Q = np.concatenate([w.Q, np.array([[1.5, -0.2], [10.0, 10.0], [-3.0, 0.5], [0.5, 1.0000001]],
+                                      dtype=np.float32)])
+    widths = np.full(2, 1.0 / 820)
+    params = ghn.GridParams(widths, w.X.min(0), np.full(2, 820))
+    index = ghn.build_arrays(w.X, w.y, params=params)
+    ref = oracle.COracle(w.X, widths)
+    _check_predict(ghn, index, ref, w.X, w.y, Q, k, "heuristic")
+    if k == 16:
+        _check_predict(ghn, index, ref, w.X, w.y, Q[:20000], k, "guaranteed")
+        _check_knn(ghn, index, ref, Q[:20000], k, "heuristic")
+
+
+def test_duplicate_points_fall_back_exactly(ghn):
+    """Many exact duplicates: equal keys the radix select cannot split go to the
+    generic kernel; ties are broken by point index exactly."""
+    rng = np.random.default_rng(5)
+    X = rng.random((200_000, 2), dtype=np.float32)
+    X[::7] = X[3]                          # 28.6k copies of one point
+    X[1::11] = np.float32(0.25)            # and a diagonal of copies
+    y = rng.integers(0, 3, X.shape[0]).astype(np.int32)
+    Q = np.concatenate([rng.random((40_000, 2), dtype=np.float32), np.repeat(X[3:4], 100, 0)])
+    index = ghn.build_arrays(X, y, cells_per_axis=256)
+    ref = oracle.COracle(X, np.full(2, 1.0 / 256))
+    for k in (3, 16):
+        _check_predict(ghn, index, ref, X, y, Q, k, "heuristic")
+
+
+@pytest.mark.parametrize("cfg,nq", [(1, 30_000), (2, 400)])
+def test_cfg1_cfg2_generic_kernel(ghn, cfg, nq):
+    from paper_2004_02290_b200 import datagen
+
+    n = 2_000_000 if cfg == 1 else 1_000_000
+    w = datagen.make(cfg, n=n, nq=nq)
+    index = ghn.build_arrays(w.X, w.y, cells_per_axis=w.cells_per_axis)
+    ref = oracle.COracle(w.X, w.widths)
+    order, cids, starts, _, _ = ref.export()
+    assert np.array_equal(index.order, order)
+    assert np.array_equal(index.cell_array, cids)
+    task = "regress" if w.task == "regress" else "classify"
+    _check_predict(ghn, index, ref, w.X, w.y, w.Q, w.k, "heuristic", task=task)
+    _check_knn(ghn, index, ref, w.Q[:200], w.k, "heuristic")
