@@ -116,6 +116,7 @@ typedef struct ghn_index_view {
     const int32_t *labels;       /* original point order; classify only */
     const double *targets;       /* original point order; regress only */
     const int32_t *labels_perm;  /* labels in CSR slot order (ghn_gather_i32), or NULL */
+    int32_t n_labels;            /* label codes lie in [0, n_labels), or 0 if unknown */
 } ghn_index_view;
 
 typedef struct ghn_query_out {

@@ -65,6 +65,7 @@ class IndexView(ctypes.Structure):
         ("ext", _i64 * GHN_MAX_DIM),
         ("coords", _p), ("perm", _p), ("cell_start", _p), ("cell_ids", _p),
         ("pt_off", _p), ("ne_off", _p), ("labels", _p), ("targets", _p), ("labels_perm", _p),
+        ("n_labels", _i32),
     ]
 
 

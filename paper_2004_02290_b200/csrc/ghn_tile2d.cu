@@ -24,6 +24,7 @@
 // a fallback list and answered by the generic warp-per-query kernel.
 #include <math.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include "ghn_common.cuh"
@@ -62,6 +63,8 @@ struct T2Args {
     unsigned long long *totals;
     int32_t *fb_list;
     int32_t *fb_count;
+    int32_t dbg;
+    int32_t small_labels;
 };
 
 struct Win {
@@ -163,6 +166,7 @@ struct Kth {
 // Per-warp shared scratch.
 struct WarpScratch {
     int hist[32];
+    int lcnt[32];     // vote counters when every label code is in [0, 32)
     double bkey[32];
     int32_t bidx[32];
     int32_t bg[32];
@@ -204,42 +208,93 @@ __device__ __forceinline__ bool lt_pair(double ka, int32_t ia, double kb, int32_
     return ka < kb || (ka == kb && ia < ib);
 }
 
-// Radix select over the candidates of `rg` with key in [lo, hi]: the r-th
-// smallest (key, index) and the vote over the r members.  Level-1 buckets on
-// the monotone fp32 round-down of the key (32 buckets, one per lane), a
-// level-2 split of the boundary bucket when it holds more than 32, then the
-// boundary candidates are ranked exactly.  False = cannot resolve.
-__device__ __forceinline__ bool select_vote_w(const T2Args &a, const Win &w, WarpScratch &sc,
-                                              const Ranges &rg, double q0, double q1, int r,
-                                              double lo, double hi, Kth &out, VoteW &v) {
+// A candidate set: the flattened ranges of a block; keys are recomputed
+// from the staged coordinates on every pass (cheaper than holding them:
+// this kernel is latency-bound and occupancy-limited).
+struct Cands {
+    const Win *w;
+    const Ranges *rg;
+    double q0, q1;
+    int nch;   // warp-uniform number of 32-candidate chunks
+    // candidate i*32 + lane: key and global slot (-1 = absent)
+    __device__ __forceinline__ void at(int i, double &key, int32_t &g) const {
+        int p, row;
+        key = INFINITY;
+        g = -1;
+        if (ranges_at(*rg, i * 32 + lane_id(), p, row)) {
+            key = key2(*w, p, q0, q1);
+            g = p + w->delta[row];
+        }
+    }
+};
+
+__device__ __forceinline__ Cands make_cands(const Win &w, const Ranges &rg, double q0, double q1) {
+    Cands c;
+    c.w = &w;
+    c.rg = &rg;
+    c.q0 = q0;
+    c.q1 = q1;
+    c.nch = (rg.total + 31) >> 5;
+    return c;
+}
+
+// Count member lanes into the vote: shared counters when labels are small
+// codes, else the general per-lane table.
+__device__ __forceinline__ void vote_members(const T2Args &a, WarpScratch &sc, VoteW &v, bool small,
+                                             bool member, int32_t g) {
+    const unsigned mem = __ballot_sync(GHN_FULL, member);
+    if (!mem) return;
+    const int32_t L = member ? a.labels_perm[g] : -1;
+    if (small) {
+        if (member) {
+            const unsigned grp = __match_any_sync(mem, L);
+            if ((grp & lanemask_lt()) == 0) atomicAdd(&sc.lcnt[L], __popc(grp));
+        }
+    } else {
+        vote_lanes(v, mem, L);
+    }
+}
+
+// Radix select over cached candidates with key in [lo, hi]: the r-th smallest
+// (key, index) and the vote over the r members.  Level-1 buckets on the
+// monotone fp32 round-down of the key (32 buckets, one per lane), a level-2
+// split of the boundary bucket when it holds more than 32, then the boundary
+// candidates are ranked exactly.  False = cannot resolve.
+__device__ __forceinline__ bool select_vote_c(const T2Args &a, WarpScratch &sc, const Cands &c, int r,
+                                              double lo, double hi, Kth &out, VoteW &v,
+                                              int32_t og0 = 0, int32_t og1 = 0x7fffffff,
+                                              bool *outside = nullptr) {
     const int lane = lane_id();
+    const bool small = a.small_labels != 0;
     const float flo = __double2float_rd(lo);
     const float fhi = __double2float_ru(hi);
     const float sc1 = fhi > flo ? fminf(32.0f * __frcp_rn(fhi - flo), 1e30f) : 0.0f;
 #define T2_B1(k32) min((int)(((k32) - flo) * sc1), 31)
     sc.hist[lane] = 0;
+    sc.lcnt[lane] = 0;
     __syncwarp();
-    for (int base = 0; base < rg.total; base += 32) {
-        int p, row;
-        const bool act = ranges_at(rg, base + lane, p, row);
-        double key = 0.0;
-        if (act) key = key2(w, p, q0, q1);
-        const bool in = act && key >= lo && key <= hi;
-        const int b = in ? T2_B1(__double2float_rd(key)) : -1;
-        const unsigned im = __ballot_sync(GHN_FULL, in);
-        if (in) {
-            const unsigned grp = __match_any_sync(im, b);
-            if ((grp & lanemask_lt()) == 0) atomicAdd(&sc.hist[b], __popc(grp));
+    for (int i = 0; i < c.nch; ++i) {
+        {
+            double ckey;
+            int32_t cgs;
+            c.at(i, ckey, cgs);
+            const bool in = cgs >= 0 && ckey >= lo && ckey <= hi;
+            const int b = in ? T2_B1(__double2float_rd(ckey)) : -1;
+            const unsigned im = __ballot_sync(GHN_FULL, in);
+            if (in) {
+                const unsigned grp = __match_any_sync(im, b);
+                if ((grp & lanemask_lt()) == 0) atomicAdd(&sc.hist[b], __popc(grp));
+            }
         }
     }
     __syncwarp();
-    int c = sc.hist[lane];
-    int incl = warp_inclusive_scan(c);
+    int cnt = sc.hist[lane];
+    int incl = warp_inclusive_scan(cnt);
     unsigned ge = __ballot_sync(GHN_FULL, incl >= r);
     if (!ge) return false;
     const int bs1 = __ffs(ge) - 1;
-    int m = __shfl_sync(GHN_FULL, c, bs1);
-    r -= __shfl_sync(GHN_FULL, incl - c, bs1);
+    int m = __shfl_sync(GHN_FULL, cnt, bs1);
+    r -= __shfl_sync(GHN_FULL, incl - cnt, bs1);
     int bs2 = -1;
     float lo2 = 0.0f, sc2 = 0.0f;
     if (m > 32) {
@@ -249,75 +304,71 @@ __device__ __forceinline__ bool select_vote_w(const T2Args &a, const Win &w, War
         __syncwarp();
         sc.hist[lane] = 0;
         __syncwarp();
-        for (int base = 0; base < rg.total; base += 32) {
-            int p, row;
-            const bool act = ranges_at(rg, base + lane, p, row);
-            double key = 0.0;
-            if (act) key = key2(w, p, q0, q1);
-            bool in = act && key >= lo && key <= hi;
-            int b = -1;
-            if (in) {
-                const float k32 = __double2float_rd(key);
-                in = T2_B1(k32) == bs1;
-                b = T2_B2(k32);
-            }
-            const unsigned im = __ballot_sync(GHN_FULL, in);
-            if (in) {
-                const unsigned grp = __match_any_sync(im, b);
-                if ((grp & lanemask_lt()) == 0) atomicAdd(&sc.hist[b], __popc(grp));
+        for (int i = 0; i < c.nch; ++i) {
+            {
+                double ckey;
+                int32_t cgs;
+                c.at(i, ckey, cgs);
+                bool in = cgs >= 0 && ckey >= lo && ckey <= hi;
+                int b = -1;
+                if (in) {
+                    const float k32 = __double2float_rd(ckey);
+                    in = T2_B1(k32) == bs1;
+                    b = T2_B2(k32);
+                }
+                const unsigned im = __ballot_sync(GHN_FULL, in);
+                if (in) {
+                    const unsigned grp = __match_any_sync(im, b);
+                    if ((grp & lanemask_lt()) == 0) atomicAdd(&sc.hist[b], __popc(grp));
+                }
             }
         }
         __syncwarp();
-        c = sc.hist[lane];
-        incl = warp_inclusive_scan(c);
+        cnt = sc.hist[lane];
+        incl = warp_inclusive_scan(cnt);
         ge = __ballot_sync(GHN_FULL, incl >= r);
         if (!ge) return false;
         bs2 = __ffs(ge) - 1;
-        m = __shfl_sync(GHN_FULL, c, bs2);
-        r -= __shfl_sync(GHN_FULL, incl - c, bs2);
+        m = __shfl_sync(GHN_FULL, cnt, bs2);
+        r -= __shfl_sync(GHN_FULL, incl - cnt, bs2);
         if (m > 32) return false;
     }
-    // collect: members below the boundary vote now; boundary candidates are
-    // compacted into the scratch and ranked exactly afterwards
+    // members below the boundary vote now; boundary candidates are compacted
     v.lab = 0;
     v.cnt = 0;
     v.used = 0;
     v.overflow = false;
     int nb = 0;
-    for (int base = 0; base < rg.total; base += 32) {
-        int p, row;
-        const bool act = ranges_at(rg, base + lane, p, row);
-        double key = 0.0;
-        if (act) key = key2(w, p, q0, q1);
-        int side = 1;
-        if (act && key >= lo && key <= hi) {
-            const float k32 = __double2float_rd(key);
-            const int b1 = T2_B1(k32);
-            side = b1 < bs1 ? -1 : (b1 > bs1 ? 1 : 0);
-            if (side == 0 && bs2 >= 0) {
-                const int b2 = T2_B2(k32);
-                side = b2 < bs2 ? -1 : (b2 > bs2 ? 1 : 0);
+    for (int i = 0; i < c.nch; ++i) {
+        {
+            double ckey;
+            int32_t cgs;
+            c.at(i, ckey, cgs);
+            int side = 1;
+            if (cgs >= 0 && ckey >= lo && ckey <= hi) {
+                const float k32 = __double2float_rd(ckey);
+                const int b1 = T2_B1(k32);
+                side = b1 < bs1 ? -1 : (b1 > bs1 ? 1 : 0);
+                if (side == 0 && bs2 >= 0) {
+                    const int b2 = T2_B2(k32);
+                    side = b2 < bs2 ? -1 : (b2 > bs2 ? 1 : 0);
+                }
             }
+            vote_members(a, sc, v, small, side < 0, cgs);
+            if (outside && __any_sync(GHN_FULL, side < 0 && (cgs < og0 || cgs >= og1))) *outside = true;
+            const unsigned bnd = __ballot_sync(GHN_FULL, side == 0);
+            if (side == 0) {
+                const int pos = nb + __popc(bnd & lanemask_lt());
+                sc.bkey[pos] = ckey;
+                sc.bidx[pos] = a.perm[cgs];
+                sc.bg[pos] = cgs;
+            }
+            nb += __popc(bnd);
         }
-        const int32_t g = p + w.delta[row];
-        const unsigned mem = __ballot_sync(GHN_FULL, side < 0);
-        if (mem) {
-            const int32_t L = side < 0 ? a.labels_perm[g] : 0;
-            vote_lanes(v, mem, L);
-        }
-        const unsigned bnd = __ballot_sync(GHN_FULL, side == 0);
-        if (side == 0) {
-            const int pos = nb + __popc(bnd & lanemask_lt());
-            sc.bkey[pos] = key;
-            sc.bidx[pos] = a.perm[g];
-            sc.bg[pos] = g;
-        }
-        nb += __popc(bnd);
     }
 #undef T2_B1
 #undef T2_B2
     __syncwarp();
-    // rank the nb (== m) boundary candidates exactly
     double mk = INFINITY;
     int32_t mi = 0x7fffffff, mg = 0;
     if (lane < nb) {
@@ -331,58 +382,59 @@ __device__ __forceinline__ bool select_vote_w(const T2Args &a, const Win &w, War
         const int32_t ti = __shfl_sync(GHN_FULL, mi, t);
         rank += lt_pair(tk, ti, mk, mi) ? 1 : 0;
     }
-    const bool memb = lane < nb && rank < r;
-    const unsigned bm = __ballot_sync(GHN_FULL, memb);
-    if (bm) vote_lanes(v, bm, memb ? a.labels_perm[mg] : 0);
+    vote_members(a, sc, v, small, lane < nb && rank < r, mg);
+    if (outside && __any_sync(GHN_FULL, lane < nb && rank < r && (mg < og0 || mg >= og1))) *outside = true;
     const unsigned kl = __ballot_sync(GHN_FULL, lane < nb && rank == r - 1);
     if (!kl) return false;
     const int src = __ffs(kl) - 1;
     out.key = __shfl_sync(GHN_FULL, mk, src);
     out.idx = __shfl_sync(GHN_FULL, mi, src);
     __syncwarp();
+    if (small) {   // counters -> table: lane j holds label j
+        v.lab = lane;
+        v.cnt = sc.lcnt[lane];
+        v.used = 32;
+    }
     return !v.overflow;
 }
 
 // Tie-break among the labels tied at the top count: the label of the member
-// minimising (sqrt(key), index) (predict.py:30-35), over the k members.
-__device__ __forceinline__ int32_t vote_tiebreak(const T2Args &a, const Win &w, const Ranges &rg,
-                                                 double q0, double q1, const Kth &kth, const VoteW &v,
-                                                 int top) {
+// minimising (sqrt(key), index) (predict.py:30-35), over the cached members.
+__device__ __forceinline__ int32_t vote_tiebreak_c(const T2Args &a, const Cands &c, const Kth &kth,
+                                                   const VoteW &v, int top) {
     const int lane = lane_id();
-    double bd = INFINITY, bkey = INFINITY;
+    // tied labels, one per lane of the table
+    const bool my_tied = lane < v.used && v.cnt == top;
+    double bd = INFINITY;
     int32_t bi = 0x7fffffff, bl = 0;
-    for (int base = 0; base < rg.total; base += 32) {
-        int p, row;
-        const bool act = ranges_at(rg, base + lane, p, row);
-        double key = INFINITY;
-        int32_t idx = 0x7fffffff, L = 0;
-        bool member = false;
-        if (act) {
-            key = key2(w, p, q0, q1);
-            const int32_t g = p + w.delta[row];
-            if (key <= kth.key) {
-                idx = a.perm[g];
+    for (int i = 0; i < c.nch; ++i) {
+        {
+            double key;
+            int32_t cgs;
+            c.at(i, key, cgs);
+            int32_t idx = 0x7fffffff, Lb = -1;
+            bool member = false;
+            if (cgs >= 0 && key <= kth.key) {
+                idx = a.perm[cgs];
                 member = key < kth.key || idx <= kth.idx;
-                if (member) L = a.labels_perm[g];
+                if (member) Lb = a.labels_perm[cgs];
             }
-        }
-        bool tied = false;
-        for (int t = 0; t < v.used; ++t) {
-            const int32_t tl = __shfl_sync(GHN_FULL, v.lab, t);
-            const int32_t tc = __shfl_sync(GHN_FULL, v.cnt, t);
-            tied |= member && tl == L && tc == top;
-        }
-        if (tied) {
-            const double dd = sqrt(key);
-            if (dd < bd || (dd == bd && idx < bi)) {
-                bd = dd;
-                bi = idx;
-                bl = L;
-                bkey = key;
+            bool tied = false;
+            for (int t = 0; t < v.used; ++t) {
+                const int32_t tl = __shfl_sync(GHN_FULL, v.lab, t);
+                const bool tt = __shfl_sync(GHN_FULL, my_tied, t);
+                tied |= member && tt && tl == Lb;
+            }
+            if (tied) {
+                const double dd = sqrt(key);
+                if (dd < bd || (dd == bd && idx < bi)) {
+                    bd = dd;
+                    bi = idx;
+                    bl = Lb;
+                }
             }
         }
     }
-    (void)bkey;
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) {
         const double od = __shfl_xor_sync(GHN_FULL, bd, off);
@@ -417,6 +469,96 @@ __device__ __forceinline__ int block_cells(const Win &w, int lr, int lc, int l) 
     return warp_sum(cells);
 }
 
+// k = 1: the top-1 is a running minimum; a layer `changed` iff its minimum
+// (key, index) precedes the current one (explore.py:112-119 with k = 1).
+__device__ __forceinline__ void process_query_k1(const T2Args &a, const Win &w, double q0, double q1,
+                                                 int32_t qi, int lr, int lc, int lmax, bool want_stats) {
+    const int lane = lane_id();
+    double ck = INFINITY;
+    int32_t ci = 0x7fffffff, cg = -1;
+    bool have = false;
+    int64_t points = 0;
+    int layers = 0;
+    for (int l = 0;; ++l) {
+        if (l > a.A) {
+            if (lane == 0) push_fallback(a, qi);
+            return;
+        }
+        const Ranges rg = l == 0 ? block_ranges(w, lr, lc, 0) : shell_ranges(w, lr, lc, l);
+        // per-lane minimum by key, index resolved for the lane's winner / ties
+        double mk = INFINITY;
+        int32_t mg = -1, mi = 0x7fffffff;
+        for (int base = 0; base < rg.total; base += 32) {
+            int p, row;
+            if (ranges_at(rg, base + lane, p, row)) {
+                const double key = key2(w, p, q0, q1);
+                const int32_t g = p + w.delta[row];
+                if (key < mk) {
+                    mk = key;
+                    mg = g;
+                    mi = 0x7fffffff;
+                } else if (key == mk) {
+                    if (mi == 0x7fffffff) mi = a.perm[mg];
+                    const int32_t ii = a.perm[g];
+                    if (ii < mi) {
+                        mi = ii;
+                        mg = g;
+                    }
+                }
+            }
+        }
+        if (mg >= 0 && mi == 0x7fffffff) mi = a.perm[mg];
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            const double ok = __shfl_xor_sync(GHN_FULL, mk, off);
+            const int32_t oi = __shfl_xor_sync(GHN_FULL, mi, off);
+            const int32_t og = __shfl_xor_sync(GHN_FULL, mg, off);
+            if (lt_pair(ok, oi, mk, mi)) {
+                mk = ok;
+                mi = oi;
+                mg = og;
+            }
+        }
+        points += rg.total;
+        layers = l;
+        bool changed = false;
+        if (rg.total > 0 && (!have || lt_pair(mk, mi, ck, ci))) {
+            ck = mk;
+            ci = mi;
+            cg = mg;
+            changed = true;
+            have = true;
+        }
+        bool stop = false;
+        if (have) {
+            if (a.mode == GHN_MODE_HEURISTIC && !changed) stop = true;
+            if (a.mode == GHN_MODE_GUARANTEED) {
+                const double b = __dmul_rn((double)l, a.min_w);
+                if (__dmul_rn(b, b) > ck) stop = true;
+            }
+        }
+        if (stop || l >= lmax) break;
+    }
+    const int64_t cells = want_stats ? block_cells(w, lr, lc, layers) : 0;
+    if (lane == 0) {
+        if (a.out_label) a.out_label[qi] = a.labels_perm[cg];
+        if (a.out_conf) a.out_conf[qi] = 1.0;
+        if (want_stats) {
+            if (a.out_stats) {
+                a.out_stats[3 * (int64_t)qi + 0] = layers;
+                a.out_stats[3 * (int64_t)qi + 1] = cells;
+                a.out_stats[3 * (int64_t)qi + 2] = points;
+            }
+            if (a.totals) {
+                atomicAdd(&a.totals[0], (unsigned long long)layers);
+                atomicAdd(&a.totals[1], (unsigned long long)cells);
+                atomicAdd(&a.totals[2], (unsigned long long)points);
+                atomicAdd(&a.totals[3], 1ull);
+            }
+        }
+    }
+}
+
 __device__ __forceinline__ void process_query_w(const T2Args &a, const Win &w, WarpScratch &sc, int qq,
                                                 int t0, int t1, int r_lo, int c_lo, bool want_stats) {
     const int lane = lane_id();
@@ -440,6 +582,10 @@ __device__ __forceinline__ void process_query_w(const T2Args &a, const Win &w, W
     const int lr = (int)(cc0 - r_lo), lc = (int)(cc1 - c_lo);
     const int lmax = max(max((int)cc0, a.ext0 - 1 - (int)cc0), max((int)cc1, a.ext1 - 1 - (int)cc1));
     const int k = a.k;
+    if (k == 1 && a.dbg == 0) {
+        process_query_k1(a, w, q0, q1, qi, lr, lc, lmax, want_stats);
+        return;
+    }
     // phase 1: whole layers enter while fewer than k points are buffered
     int l = 0;
     Ranges blk;
@@ -451,26 +597,53 @@ __device__ __forceinline__ void process_query_w(const T2Args &a, const Win &w, W
         blk = block_ranges(w, lr, lc, l);
         if (blk.total >= k || l >= lmax) break;
     }
-    int64_t points = blk.total;
-    int64_t cells = want_stats ? block_cells(w, lr, lc, l) : 0;
-    int layers = l;
+    if (a.dbg == 1) {
+        if (lane == 0 && a.out_label) a.out_label[qi] = blk.total;
+        return;
+    }
+    bool stop = a.dbg == 2;
     Kth kth{INFINITY, 0x7fffffff};
     VoteW v{0, 0, 0, false};
-    {
-        const double e0 = fmax(q0 - (double)(a.lo0 + cc0 - l) * a.w0, (double)(a.lo0 + cc0 + l + 1) * a.w0 - q0);
-        const double e1 = fmax(q1 - (double)(a.lo1 + cc1 - l) * a.w1, (double)(a.lo1 + cc1 + l + 1) * a.w1 - q1);
+    if (l == 0 && lmax >= 1 && a.A >= 1 && a.dbg != 2) {
+        // Layer 0 filled the buffer and always `changed`; neither stop rule can
+        // fire at l = 0, so T_0 is never needed: select T_1 over block(1)
+        // directly.  changed(1) <=> a member of T_1 lies outside the centre cell.
+        const int32_t *rp = w.loc + lr * w.W1;
+        const int32_t og0 = rp[lc] + w.delta[lr], og1 = rp[lc + 1] + w.delta[lr];
+        l = 1;
+        blk = block_ranges(w, lr, lc, 1);
+        const double e0 = fmax(q0 - (double)(a.lo0 + cc0 - 1) * a.w0, (double)(a.lo0 + cc0 + 2) * a.w0 - q0);
+        const double e1 = fmax(q1 - (double)(a.lo1 + cc1 - 1) * a.w1, (double)(a.lo1 + cc1 + 2) * a.w1 - q1);
         const double hi = (e0 * e0 + e1 * e1) * (1.0 + 1e-6) + 1e-300;
-        if (blk.total < k || !select_vote_w(a, w, sc, blk, q0, q1, k, 0.0, hi, kth, v)) {
+        const Cands cd = make_cands(w, blk, q0, q1);
+        bool outside = false;
+        if (!select_vote_c(a, sc, cd, k, 0.0, hi, kth, v, og0, og1, &outside)) {
             if (lane == 0) push_fallback(a, qi);
             return;
         }
+        if (a.mode == GHN_MODE_HEURISTIC && !outside) stop = true;
+        if (a.mode == GHN_MODE_GUARANTEED) {
+            const double b = __dmul_rn(1.0, a.min_w);
+            if (__dmul_rn(b, b) > kth.key) stop = true;
+        }
+    } else {
+        const double e0 = fmax(q0 - (double)(a.lo0 + cc0 - l) * a.w0, (double)(a.lo0 + cc0 + l + 1) * a.w0 - q0);
+        const double e1 = fmax(q1 - (double)(a.lo1 + cc1 - l) * a.w1, (double)(a.lo1 + cc1 + l + 1) * a.w1 - q1);
+        const double hi = (e0 * e0 + e1 * e1) * (1.0 + 1e-6) + 1e-300;
+        const Cands cd = make_cands(w, blk, q0, q1);
+        if (blk.total < k || !select_vote_c(a, sc, cd, k, 0.0, hi, kth, v)) {
+            if (lane == 0) push_fallback(a, qi);
+            return;
+        }
+        // the layer that filled the buffer `changed`; the guaranteed bound may stop
+        if (a.mode == GHN_MODE_GUARANTEED) {
+            const double b = __dmul_rn((double)l, a.min_w);
+            if (__dmul_rn(b, b) > kth.key) stop = true;
+        }
     }
-    // the layer that filled the buffer `changed`; the guaranteed bound may stop
-    bool stop = false;
-    if (a.mode == GHN_MODE_GUARANTEED) {
-        const double b = __dmul_rn((double)l, a.min_w);
-        if (__dmul_rn(b, b) > kth.key) stop = true;
-    }
+    int64_t points = blk.total;
+    int64_t cells = want_stats ? block_cells(w, lr, lc, l) : 0;
+    int layers = l;
     // phase 2: a later layer matters only if one of its points precedes the k-th
     while (!stop && l < lmax) {
         ++l;
@@ -496,7 +669,8 @@ __device__ __forceinline__ void process_query_w(const T2Args &a, const Win &w, W
         const bool changed = below > 0;
         if (changed) {
             blk = block_ranges(w, lr, lc, l);
-            if (!select_vote_w(a, w, sc, blk, q0, q1, k, 0.0, kth.key, kth, v)) {
+            const Cands cd = make_cands(w, blk, q0, q1);
+            if (!select_vote_c(a, sc, cd, k, 0.0, kth.key, kth, v)) {
                 if (lane == 0) push_fallback(a, qi);
                 return;
             }
@@ -513,7 +687,8 @@ __device__ __forceinline__ void process_query_w(const T2Args &a, const Win &w, W
     int32_t wl = __shfl_sync(GHN_FULL, v.lab, __ffs(tiedm) - 1);
     if (__popc(tiedm) > 1) {
         // members are the candidates of the last selected block
-        wl = vote_tiebreak(a, w, blk, q0, q1, kth, v, top);
+        const Cands cd = make_cands(w, blk, q0, q1);
+        wl = vote_tiebreak_c(a, cd, kth, v, top);
     }
     if (lane == 0) {
         if (a.out_label) a.out_label[qi] = wl;
@@ -553,15 +728,22 @@ __global__ void __launch_bounds__(T2_THREADS) tile2d_kernel(const T2Args a) {
         loc[e] = a.pt_off[(int64_t)(r_lo + i) * a.ext1 + c_lo + j];
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-        int s = 0;
-        for (int i = 0; i < R; ++i) {
-            rstart[i] = s;
-            delta[i] = loc[i * W1] - s;
-            s += loc[i * W1 + W] - loc[i * W1];
+    if (threadIdx.x < 32) {   // row prefix by one warp, 32 rows at a time
+        int carry = 0;
+        for (int i0 = 0; i0 < R; i0 += 32) {
+            const int i = i0 + (int)threadIdx.x;
+            const int len = i < R ? loc[i * W1 + W] - loc[i * W1] : 0;
+            const int inc = warp_inclusive_scan(len);
+            if (i < R) {
+                rstart[i] = carry + inc - len;
+                delta[i] = loc[i * W1] - (carry + inc - len);
+            }
+            carry += __shfl_sync(GHN_FULL, inc, 31);
         }
-        rstart[R] = s;
-        s_P = s;
+        if (threadIdx.x == 0) {
+            rstart[R] = carry;
+            s_P = carry;
+        }
     }
     __syncthreads();
     const int P = s_P;
@@ -570,16 +752,12 @@ __global__ void __launch_bounds__(T2_THREADS) tile2d_kernel(const T2Args a) {
         return;
     }
     for (int e = threadIdx.x; e < R * W1; e += blockDim.x) loc[e] -= delta[e / W1];
-    for (int p = threadIdx.x; p < P; p += blockDim.x) {
-        int lo = 0, hi = R - 1;
-        while (lo < hi) {
-            const int mid = (lo + hi + 1) >> 1;
-            if (rstart[mid] <= p) lo = mid;
-            else hi = mid - 1;
+    for (int i = threadIdx.x >> 5; i < R; i += T2_THREADS / 32) {   // warp per row: coalesced copy
+        const int p0 = rstart[i], p1 = rstart[i + 1], d = delta[i];
+        for (int p = p0 + (int)(threadIdx.x & 31); p < p1; p += 32) {
+            sx[p] = a.c0[p + d];
+            sy[p] = a.c1[p + d];
         }
-        const int32_t g = p + delta[lo];
-        sx[p] = a.c0[g];
-        sy[p] = a.c1[g];
     }
     __syncthreads();
     Win w{sx, sy, loc, delta, R, W, W1};
@@ -723,6 +901,8 @@ int32_t tile2d_run(const ghn_index_view *ix, const Tile2dPlan *plan, const void 
     a.totals = out->totals;
     a.fb_list = fbl;
     a.fb_count = fbc;
+    a.dbg = getenv("GHN_DEBUG_MODE") ? atoi(getenv("GHN_DEBUG_MODE")) : 0;
+    a.small_labels = ix->n_labels > 0 && ix->n_labels <= 32;
     static bool attr_set = false;
     if (!attr_set) {
         GHN_CUDA_CHECK(cudaFuncSetAttribute(tile2d_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -108,6 +108,16 @@ class _Labels:
             except (TypeError, ValueError):
                 self.targets = None
 
+    @property
+    def n_codes(self) -> int:
+        """Codes lie in [0, n_codes) (0 = unknown / negative codes)."""
+        if not hasattr(self, "_n_codes"):
+            self._n_codes = 0
+            if self.codes is not None and self.codes.numel():
+                lo, hi = int(self.codes.min()), int(self.codes.max())
+                self._n_codes = hi + 1 if lo >= 0 and hi < 2**31 - 1 else 0
+        return self._n_codes
+
     def label_of(self, code: int):
         return self.decode[code] if self.decode is not None else code
 
@@ -223,6 +233,7 @@ class GridIndex:
         v.labels = _lib.ptr(self._labels.codes)
         v.targets = _lib.ptr(self._labels.targets)
         v.labels_perm = _lib.ptr(self.labels_perm)
+        v.n_labels = self._labels.n_codes
         return v
 
 
