@@ -84,6 +84,8 @@ typedef struct ghn_fit_out {
     int32_t *n_cells;     /* scalar C_ne */
     int32_t *pt_off;      /* DENSE: slots before linear cell key c (E+1) */
     int32_t *ne_off;      /* DENSE: non-empty cells before linear cell key c (E+1) */
+    const int32_t *labels_in;  /* optional: label codes in input order */
+    int32_t *labels_perm;      /* optional: labels_in gathered into CSR slot order */
 } ghn_fit_out;
 
 /* Phase 2: stable LSD radix sort by cell (ties keep input order, as the

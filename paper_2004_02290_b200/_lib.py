@@ -51,7 +51,7 @@ class FitPlan(ctypes.Structure):
 class FitOut(ctypes.Structure):
     _fields_ = [
         ("perm", _p), ("coords", _p), ("cell_start", _p), ("cell_ids", _p), ("n_cells", _p),
-        ("pt_off", _p), ("ne_off", _p),
+        ("pt_off", _p), ("ne_off", _p), ("labels_in", _p), ("labels_perm", _p),
     ]
 
 

@@ -266,16 +266,26 @@ __global__ void pt_off_kernel(const int32_t *__restrict__ ne_off, const int32_t 
         pt_off[c] = cell_start[ne_off[c]];
 }
 
-// Permuted SoA coordinates.
+// Permuted SoA coordinates (+ labels in slot order when requested): one
+// random gather per point; a point's d coordinates are adjacent in X.
 template <typename T>
 __global__ void __launch_bounds__(FIT_THREADS) gather_coords_kernel(const T *__restrict__ X, int64_t n,
                                                                     int d,
                                                                     const int32_t *__restrict__ perm,
-                                                                    T *__restrict__ out) {
+                                                                    T *__restrict__ out,
+                                                                    const int32_t *__restrict__ lab_in,
+                                                                    int32_t *__restrict__ lab_out) {
     for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < n;
          s += (int64_t)gridDim.x * blockDim.x) {
-        int64_t src = perm[s];
-        for (int j = 0; j < d; ++j) out[(int64_t)j * n + s] = X[src * d + j];
+        const int64_t src = perm[s];
+        if (d == 2 && sizeof(T) == 4) {
+            const float2 v = reinterpret_cast<const float2 *>(X)[src];
+            out[s] = (T)v.x;
+            out[n + s] = (T)v.y;
+        } else {
+            for (int j = 0; j < d; ++j) out[(int64_t)j * n + s] = X[src * d + j];
+        }
+        if (lab_out) lab_out[s] = lab_in[src];
     }
 }
 
@@ -378,7 +388,8 @@ int32_t fit_build_impl(const ghn_fit_plan *plan, const T *X, const ghn_fit_out *
                                                        out->cell_ids, out->n_cells);
         GHN_LAUNCH_CHECK("list_emit_kernel");
     }
-    gather_coords_kernel<T><<<g, FIT_THREADS, 0, s>>>(X, n, d, out->perm, (T *)out->coords);
+    gather_coords_kernel<T><<<g, FIT_THREADS, 0, s>>>(X, n, d, out->perm, (T *)out->coords,
+                                                       out->labels_in, out->labels_perm);
     GHN_LAUNCH_CHECK("gather_coords_kernel");
     (void)ws_bytes;
     return GHN_OK;

@@ -469,10 +469,40 @@ __device__ __forceinline__ int block_cells(const Win &w, int lr, int lc, int l) 
     return warp_sum(cells);
 }
 
+// Every point of shell(l+1) lies outside block(l), so its distance to q is at
+// least the distance from q to the nearest face of block(l).  When that bound
+// (less a rounding margin far above fp64 error: cell assignment by floor(x/w)
+// and the key's own rounding are both within a few ulps) exceeds the k-th
+// key, no point of the shell can precede the k-th: the layer is visited
+// (counted in QueryStats) but cannot change the top-k.
+__device__ __forceinline__ bool shell_cannot_change(const T2Args &a, double q0, double q1, int64_t cc0,
+                                                    int64_t cc1, int l, double kth_key) {
+    const double f0 = fmin(q0 - (double)(a.lo0 + cc0 - l) * a.w0, (double)(a.lo0 + cc0 + l + 1) * a.w0 - q0);
+    const double f1 = fmin(q1 - (double)(a.lo1 + cc1 - l) * a.w1, (double)(a.lo1 + cc1 + l + 1) * a.w1 - q1);
+    const double margin = 1e-9 * fmax(a.w0, a.w1) + 1e-12 * (fabs(q0) + fabs(q1));
+    const double d = fmin(f0, f1) - margin;
+    if (!(d > 0.0)) return false;
+    return d * d * (1.0 - 1e-9) > kth_key;
+}
+
+// Points in block(l) (warp-uniform; one row per lane).
+__device__ __forceinline__ int block_total(const Win &w, int lr, int lc, int l) {
+    const int lane = lane_id();
+    int n = 0;
+    const int i = lr - l + lane;
+    if (lane <= 2 * l && i >= 0 && i < w.R) {
+        const int a = max(lc - l, 0), b = min(lc + l, w.W - 1);
+        const int32_t *rp = w.loc + i * w.W1;
+        n = rp[b + 1] - rp[a];
+    }
+    return warp_sum(n);
+}
+
 // k = 1: the top-1 is a running minimum; a layer `changed` iff its minimum
 // (key, index) precedes the current one (explore.py:112-119 with k = 1).
 __device__ __forceinline__ void process_query_k1(const T2Args &a, const Win &w, double q0, double q1,
-                                                 int32_t qi, int lr, int lc, int lmax, bool want_stats) {
+                                                 int32_t qi, int64_t cc0, int64_t cc1, int lr, int lc,
+                                                 int lmax, bool want_stats) {
     const int lane = lane_id();
     double ck = INFINITY;
     int32_t ci = 0x7fffffff, cg = -1;
@@ -483,6 +513,18 @@ __device__ __forceinline__ void process_query_k1(const T2Args &a, const Win &w, 
         if (l > a.A) {
             if (lane == 0) push_fallback(a, qi);
             return;
+        }
+        if (have && l > 0 && shell_cannot_change(a, q0, q1, cc0, cc1, l - 1, ck)) {
+            // shell(l) cannot hold a point preceding the current minimum
+            points += block_total(w, lr, lc, l) - block_total(w, lr, lc, l - 1);
+            layers = l;
+            bool stop = a.mode == GHN_MODE_HEURISTIC;
+            if (a.mode == GHN_MODE_GUARANTEED) {
+                const double b = __dmul_rn((double)l, a.min_w);
+                if (__dmul_rn(b, b) > ck) stop = true;
+            }
+            if (stop || l >= lmax) break;
+            continue;
         }
         const Ranges rg = l == 0 ? block_ranges(w, lr, lc, 0) : shell_ranges(w, lr, lc, l);
         // per-lane minimum by key, index resolved for the lane's winner / ties
@@ -583,7 +625,7 @@ __device__ __forceinline__ void process_query_w(const T2Args &a, const Win &w, W
     const int lmax = max(max((int)cc0, a.ext0 - 1 - (int)cc0), max((int)cc1, a.ext1 - 1 - (int)cc1));
     const int k = a.k;
     if (k == 1 && a.dbg == 0) {
-        process_query_k1(a, w, q0, q1, qi, lr, lc, lmax, want_stats);
+        process_query_k1(a, w, q0, q1, qi, cc0, cc1, lr, lc, lmax, want_stats);
         return;
     }
     // phase 1: whole layers enter while fewer than k points are buffered
@@ -651,19 +693,23 @@ __device__ __forceinline__ void process_query_w(const T2Args &a, const Win &w, W
             if (lane == 0) push_fallback(a, qi);
             return;
         }
-        const Ranges sh = shell_ranges(w, lr, lc, l);
         int below = 0;
-        for (int base = 0; base < sh.total; base += 32) {
-            int p, row;
-            const bool act = ranges_at(sh, base + lane, p, row);
-            bool lt = false;
-            if (act) {
-                const double key = key2(w, p, q0, q1);
-                lt = key < kth.key || (key == kth.key && a.perm[p + w.delta[row]] < kth.idx);
+        if (shell_cannot_change(a, q0, q1, cc0, cc1, l - 1, kth.key)) {
+            points += block_total(w, lr, lc, l) - block_total(w, lr, lc, l - 1);
+        } else {
+            const Ranges sh = shell_ranges(w, lr, lc, l);
+            for (int base = 0; base < sh.total; base += 32) {
+                int p, row;
+                const bool act = ranges_at(sh, base + lane, p, row);
+                bool lt = false;
+                if (act) {
+                    const double key = key2(w, p, q0, q1);
+                    lt = key < kth.key || (key == kth.key && a.perm[p + w.delta[row]] < kth.idx);
+                }
+                below += __popc(__ballot_sync(GHN_FULL, lt));
             }
-            below += __popc(__ballot_sync(GHN_FULL, lt));
+            points += sh.total;
         }
-        points += sh.total;
         layers = l;
         if (want_stats) cells = block_cells(w, lr, lc, l);
         const bool changed = below > 0;

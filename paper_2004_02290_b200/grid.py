@@ -64,17 +64,21 @@ class _Labels:
         self.values = values                  # python list (original objects) or None
         self.decode = None                    # code -> label (None = identity)
         self.codes = None                     # device int32 (n,)
-        self.targets = None                   # device float64 (n,)
+        self._targets = None                  # device float64 (n,), built on first use
+        self._targets_from_codes = False
         arr = None
         if isinstance(values, torch.Tensor):
             t = values.to(device)
             if t.dtype.is_floating_point:
-                self.targets = t.to(torch.float64).contiguous()
+                self._targets = t.to(torch.float64).contiguous()
             else:
-                if t.numel() and (int(t.min()) < -2**31 or int(t.max()) >= 2**31):
+                lo, hi = (torch.aminmax(t) if t.numel() else (torch.zeros(()), torch.zeros(())))
+                lo, hi = int(lo), int(hi)
+                if lo < -2**31 or hi >= 2**31:
                     raise ValueError("integer labels must fit in int32")
-                self.codes = t.to(torch.int32).contiguous()
-                self.targets = t.to(torch.float64).contiguous()
+                self.codes = t if t.dtype == torch.int32 and t.is_contiguous() else t.to(torch.int32).contiguous()
+                self._n_codes = hi + 1 if lo >= 0 and t.numel() else 0
+                self._targets_from_codes = True
             return
         try:
             arr = np.asarray(values)
@@ -88,10 +92,10 @@ class _Labels:
                 self.decode = uniq.tolist()
             else:
                 self.codes = torch.as_tensor(a64.astype(np.int32), device=device)
-            self.targets = torch.as_tensor(a64.astype(np.float64), device=device)
+            self._targets = torch.as_tensor(a64.astype(np.float64), device=device)
         elif arr is not None and arr.ndim == 1 and arr.dtype.kind == "f":
             f64 = arr.astype(np.float64)
-            self.targets = torch.as_tensor(f64, device=device)
+            self._targets = torch.as_tensor(f64, device=device)
             uniq, inv = np.unique(f64, return_inverse=True)
             self.codes = torch.as_tensor(inv.astype(np.int32), device=device)
             self.decode = uniq.tolist()
@@ -104,9 +108,18 @@ class _Labels:
             self.codes = torch.as_tensor(codes, device=device)
             self.decode = list(table.keys())
             try:
-                self.targets = torch.as_tensor(np.array([float(v) for v in values]), device=device)
+                self._targets = torch.as_tensor(np.array([float(v) for v in values]), device=device)
             except (TypeError, ValueError):
-                self.targets = None
+                self._targets = None
+
+    @property
+    def targets(self):
+        """fp64 regression targets float(label) (predict.py:43), built lazily."""
+        if self._targets is None and self._targets_from_codes:
+            import torch
+
+            self._targets = self.codes.to(torch.float64)
+        return self._targets
 
     @property
     def n_codes(self) -> int:
@@ -302,11 +315,12 @@ def build_arrays(X, y=None, params: GridParams | None = None, cells_per_axis=Non
         raise ValueError("empty dataset")
     if y is not None and len(y) != n:
         raise ValueError("labels length must match the number of rows")
+    C = None
     if params is None:
         if cells_per_axis is not None:
+            # origin (the per-dimension minimum) comes from the bounds kernel below
             C = np.broadcast_to(np.asarray(cells_per_axis, dtype=np.float64), (d,))
-            origin = Xt.to(torch.float64).min(dim=0).values.cpu().numpy() if n else np.zeros(d)
-            params = GridParams(1.0 / C, origin, C.astype(np.int64))
+            params = GridParams(1.0 / C, np.zeros(d), C.astype(np.int64))
         else:
             from .fitwidths import fit_cell_measurements_arrays
 
@@ -326,6 +340,8 @@ def build_arrays(X, y=None, params: GridParams | None = None, cells_per_axis=Non
     if int(flags.item()) & 1:
         raise ValueError("non-finite coordinate")
     bh = np.ascontiguousarray(bounds.cpu().numpy())
+    if C is not None:
+        params = GridParams(params.widths, origin.cpu().numpy(), params.splits)
     plan = _lib.FitPlan()
     _lib.check(L.ghn_fit_plan_init(ctypes.byref(plan), n, d, dtype, wptr,
                                    bh.ctypes.data_as(ctypes.c_void_p), dense_limit_for(n)),
@@ -341,20 +357,19 @@ def build_arrays(X, y=None, params: GridParams | None = None, cells_per_axis=Non
     if plan.layout == _lib.GHN_LAYOUT_DENSE:
         t["pt_off"] = torch.empty(plan.E + 1, dtype=i32, device=dev)
         t["ne_off"] = torch.empty(plan.E + 1, dtype=i32, device=dev)
+    labels = _Labels(y if y is not None else [0] * n, dev)
+    if labels.codes is not None:
+        t["labels_perm"] = torch.empty(n, dtype=i32, device=dev)   # gathered by the fit
     ws = torch.empty(plan.workspace_bytes, dtype=torch.uint8, device=dev)
     out = _lib.FitOut(
         perm=_lib.ptr(t["perm"]), coords=_lib.ptr(t["coords"]), cell_start=_lib.ptr(t["cell_start"]),
         cell_ids=_lib.ptr(t["cell_ids"]), n_cells=_lib.ptr(t["n_cells"]),
-        pt_off=_lib.ptr(t.get("pt_off")), ne_off=_lib.ptr(t.get("ne_off")))
+        pt_off=_lib.ptr(t.get("pt_off")), ne_off=_lib.ptr(t.get("ne_off")),
+        labels_in=_lib.ptr(labels.codes), labels_perm=_lib.ptr(t.get("labels_perm")))
     _lib.check(L.ghn_fit_build(ctypes.byref(plan), _lib.ptr(Xd), ctypes.byref(out), _lib.ptr(ws),
                                plan.workspace_bytes, s), "ghn_fit_build")
     n_cells = int(t["n_cells"].item())
     del ws
-    labels = _Labels(y if y is not None else [0] * n, dev)
-    if labels.codes is not None:
-        t["labels_perm"] = torch.empty(n, dtype=i32, device=dev)
-        _lib.check(L.ghn_gather_i32(_lib.ptr(labels.codes), _lib.ptr(t["perm"]), n,
-                                    _lib.ptr(t["labels_perm"]), s), "ghn_gather_i32")
     return GridIndex(params, metric, Xd, labels, plan, t, n_cells)
 
 
