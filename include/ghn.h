@@ -69,6 +69,8 @@ typedef struct ghn_fit_plan {
     int64_t lo[GHN_MAX_DIM];
     int64_t ext[GHN_MAX_DIM];         /* hi - lo + 1 */
     size_t workspace_bytes;
+    size_t fast_cursor_off;           /* counting-scatter path: workspace offsets */
+    size_t fast_rec_off;
 } ghn_fit_plan;
 
 int32_t ghn_fit_plan_init(ghn_fit_plan *plan, int64_t n, int32_t d, int32_t dtype,

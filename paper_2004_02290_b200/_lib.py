@@ -45,6 +45,8 @@ class FitPlan(ctypes.Structure):
         ("lo", _i64 * GHN_MAX_DIM),
         ("ext", _i64 * GHN_MAX_DIM),
         ("workspace_bytes", _sz),
+        ("fast_cursor_off", _sz),
+        ("fast_rec_off", _sz),
     ]
 
 

@@ -62,7 +62,7 @@ def test_plan_init_host_only():
 
 def test_struct_layouts_match_header():
     # field order / sizes mirror include/ghn.h (x86-64 LP64)
-    assert ctypes.sizeof(_lib.FitOut) == 7 * 8
+    assert ctypes.sizeof(_lib.FitOut) == 9 * 8
     assert ctypes.sizeof(_lib.QueryOut) == 7 * 8
     assert _lib.IndexView.coords.offset == 8 + 4 * 4 + 8 + 16 * 8 + 8 + 16 * 8 * 2
-    assert ctypes.sizeof(_lib.FitPlan) == 8 + 4 * 4 + 8 + 16 * 8 * 3 + 8
+    assert ctypes.sizeof(_lib.FitPlan) == 8 + 4 * 4 + 8 + 16 * 8 * 3 + 8 * 3
