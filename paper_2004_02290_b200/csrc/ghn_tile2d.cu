@@ -813,6 +813,82 @@ __global__ void __launch_bounds__(T2_THREADS) tile2d_kernel(const T2Args a) {
         process_query_w(a, w, s_scratch[warp], qq, t0, t1, r_lo, c_lo, want_stats);
 }
 
+}  // namespace
+}  // namespace ghn
+
+#include "ghn_tile2d_grp.cuh"
+
+namespace ghn {
+namespace {
+
+template <int G>
+__global__ void __launch_bounds__(T2_THREADS) tile2d_grp_kernel(const T2Args a) {
+    extern __shared__ __align__(16) unsigned char sm[];
+    __shared__ int s_P;
+    __shared__ GrpScratch s_gs[T2_THREADS / G];
+    const int t = blockIdx.x;
+    const int qb = a.tile_start[t], qe = a.tile_start[t + 1];
+    if (qb == qe) return;
+    const int t0 = t / a.nt1, t1 = t - (t / a.nt1) * a.nt1;
+    const int r_lo = max(t0 * a.T - a.A, 0), r_hi = min(t0 * a.T + a.T - 1 + a.A, a.ext0 - 1);
+    const int c_lo = max(t1 * a.T - a.A, 0), c_hi = min(t1 * a.T + a.T - 1 + a.A, a.ext1 - 1);
+    const int R = r_hi - r_lo + 1, W = c_hi - c_lo + 1, W1 = W + 1;
+    float *sx = (float *)sm;
+    float *sy = sx + T2_CAP;
+    int32_t *loc = (int32_t *)(sy + T2_CAP);                       // [R][W+1]
+    int32_t *delta = loc + a.win * (a.win + 1);                    // [R]
+    int32_t *rstart = delta + a.win;                               // [R+1]
+    for (int e = threadIdx.x; e < R * W1; e += blockDim.x) {
+        const int i = e / W1, j = e - (e / W1) * W1;
+        loc[e] = a.pt_off[(int64_t)(r_lo + i) * a.ext1 + c_lo + j];
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {   // row prefix by one warp, 32 rows at a time
+        int carry = 0;
+        for (int i0 = 0; i0 < R; i0 += 32) {
+            const int i = i0 + (int)threadIdx.x;
+            const int len = i < R ? loc[i * W1 + W] - loc[i * W1] : 0;
+            const int inc = warp_inclusive_scan(len);
+            if (i < R) {
+                rstart[i] = carry + inc - len;
+                delta[i] = loc[i * W1] - (carry + inc - len);
+            }
+            carry += __shfl_sync(GHN_FULL, inc, 31);
+        }
+        if (threadIdx.x == 0) {
+            rstart[R] = carry;
+            s_P = carry;
+        }
+    }
+    __syncthreads();
+    const int P = s_P;
+    if (P > T2_CAP) {
+        for (int qq = qb + threadIdx.x; qq < qe; qq += blockDim.x) push_fallback(a, a.qorder[qq]);
+        return;
+    }
+    for (int e = threadIdx.x; e < R * W1; e += blockDim.x) loc[e] -= delta[e / W1];
+    for (int i = threadIdx.x >> 5; i < R; i += T2_THREADS / 32) {   // warp per row: coalesced copy
+        const int p0 = rstart[i], p1 = rstart[i + 1], d = delta[i];
+        for (int p = p0 + (int)(threadIdx.x & 31); p < p1; p += 32) {
+            sx[p] = a.c0[p + d];
+            sy[p] = a.c1[p + d];
+        }
+    }
+    __syncthreads();
+    Win w{sx, sy, loc, delta, R, W, W1};
+    const Grp<G> gr;
+    const int gid = threadIdx.x / G;
+    const bool want_stats = a.out_stats != nullptr || a.totals != nullptr;
+    for (int qq = qb + gid; qq < qe; qq += T2_THREADS / G)
+        process_query_grp<G>(a, w, s_gs[gid], gr, a.qorder[qq], t0, t1, r_lo, c_lo, want_stats);
+}
+
+}  // namespace
+}  // namespace ghn
+
+namespace ghn {
+namespace {
+
 // ------------------------------------------------------------------ binning
 __global__ void tile_key_kernel(const void *Q, int32_t q_dtype, int64_t nq, double w0, double w1,
                                 double inv0, double inv1, uint32_t pow2, int64_t lo0, int64_t lo1,
@@ -872,6 +948,13 @@ bool tile2d_plan(const ghn_index_view *ix, int64_t nq, int32_t k, int32_t task, 
     plan->nt1 = (int32_t)((ix->ext[1] + T - 1) / T);
     plan->ntiles = (int64_t)plan->nt0 * plan->nt1;
     plan->win = T + 2 * A;
+    // lanes per query: k = 1 (a per-layer running minimum, no select) runs 4
+    // queries per warp; the radix select is faster warp-wide (measured: the
+    // sub-warp select loses to divergence between the groups of a warp).
+    // The group kernel votes with shared counters: label codes in [0, 32).
+    plan->G = 32;
+    if (k == 1 && ix->n_labels > 0 && ix->n_labels <= 32) plan->G = 8;
+    if (getenv("GHN_TILE_G")) plan->G = atoi(getenv("GHN_TILE_G"));
     plan->smem = (size_t)T2_CAP * 8 +
                  (size_t)plan->win * (plan->win + 1) * 4 + (size_t)plan->win * 4 +
                  (size_t)(plan->win + 1) * 4 + 64;
@@ -949,13 +1032,26 @@ int32_t tile2d_run(const ghn_index_view *ix, const Tile2dPlan *plan, const void 
     a.fb_count = fbc;
     a.dbg = getenv("GHN_DEBUG_MODE") ? atoi(getenv("GHN_DEBUG_MODE")) : 0;
     a.small_labels = ix->n_labels > 0 && ix->n_labels <= 32;
-    static bool attr_set = false;
-    if (!attr_set) {
-        GHN_CUDA_CHECK(cudaFuncSetAttribute(tile2d_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            200 * 1024));
-        attr_set = true;
+    static size_t attr_smem[3] = {0, 0, 0};   // largest dynamic smem opted into, per kernel
+    const int ki = plan->G == 8 ? 1 : (plan->G == 16 ? 2 : 0);
+    if (plan->smem > attr_smem[ki]) {
+        if (ki == 0)
+            GHN_CUDA_CHECK(cudaFuncSetAttribute(tile2d_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                (int)plan->smem));
+        else if (ki == 1)
+            GHN_CUDA_CHECK(cudaFuncSetAttribute(tile2d_grp_kernel<8>,
+                                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)plan->smem));
+        else
+            GHN_CUDA_CHECK(cudaFuncSetAttribute(tile2d_grp_kernel<16>,
+                                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)plan->smem));
+        attr_smem[ki] = plan->smem;
     }
-    tile2d_kernel<<<(unsigned)plan->ntiles, T2_THREADS, plan->smem, s>>>(a);
+    if (ki == 1)
+        tile2d_grp_kernel<8><<<(unsigned)plan->ntiles, T2_THREADS, plan->smem, s>>>(a);
+    else if (ki == 2)
+        tile2d_grp_kernel<16><<<(unsigned)plan->ntiles, T2_THREADS, plan->smem, s>>>(a);
+    else
+        tile2d_kernel<<<(unsigned)plan->ntiles, T2_THREADS, plan->smem, s>>>(a);
     GHN_LAUNCH_CHECK("tile2d_kernel");
     *fb_list = fbl;
     *fb_count = fbc;

@@ -11,6 +11,7 @@ struct Tile2dPlan {
     int32_t nt0, nt1; // tiles per dimension
     int64_t ntiles;
     int32_t win;      // T + 2A
+    int32_t G;        // lanes per query (32: warp kernel; 8/16: group kernel)
     size_t smem;      // dynamic shared memory per CTA
 };
 

@@ -107,3 +107,17 @@ def test_cfg1_cfg2_generic_kernel(ghn, cfg, nq):
     task = "regress" if w.task == "regress" else "classify"
     _check_predict(ghn, index, ref, w.X, w.y, w.Q, w.k, "heuristic", task=task)
     _check_knn(ghn, index, ref, w.Q[:200], w.k, "heuristic")
+
+
+@pytest.mark.parametrize("G", ["8", "16", "32"])
+@pytest.mark.parametrize("k", [1, 5, 16])
+def test_tiled_group_sizes_exact(ghn, G, k, monkeypatch):
+    """Every lanes-per-query variant of the tiled kernel (GHN_TILE_G) is exact."""
+    from paper_2004_02290_b200 import datagen
+
+    monkeypatch.setenv("GHN_TILE_G", G)
+    w = datagen.cfg4(n=1_000_000, nq=60_000, seed=45)
+    index = ghn.build_arrays(w.X, w.y, cells_per_axis=512)
+    ref = oracle.COracle(w.X, np.full(2, 1.0 / 512))
+    _check_predict(ghn, index, ref, w.X, w.y, w.Q, k, "heuristic")
+    _check_predict(ghn, index, ref, w.X, w.y, w.Q[:20000], k, "guaranteed")
