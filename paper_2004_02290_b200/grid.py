@@ -177,6 +177,8 @@ class GridIndex:
     @property
     def labels(self):
         v = self._labels.values
+        if isinstance(v, np.ndarray):
+            return v.tolist()
         if v is None or not isinstance(v, (list, tuple)):
             if "labels" not in self._cache:
                 src = self._labels.codes if self._labels.codes is not None else self._labels.targets

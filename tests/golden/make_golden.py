@@ -157,6 +157,17 @@ def main():
         ms = 7 if t % 7 == 6 else None
         run_case(ref, f"fit{t:02d}", X, yy, Q, k, mode, task, max_splits=ms)
 
+    # index files written by the reference's save_index (grid.py:211-246)
+    rng = np.random.default_rng(515)
+    X = rng.normal(0, 2, (120, 3))
+    pts = ref.points_from_arrays(X, list(rng.integers(0, 3, 120).tolist()))
+    ref.save_index(ref.build(pts), os.path.join(HERE, "index_fit_int.ghn"))
+    w = datagen.cfg0(n=2000, nq=10, seed=516)
+    pts = ref.points_from_arrays(w.X.astype(np.float64), [["a", "b", "c", "d"][v] for v in w.y])
+    params = ref.GridParams(w.widths, w.X.astype(np.float64).min(0), np.full(2, 32))
+    ref.save_index(ref.build(pts, params=params), os.path.join(HERE, "index_cfg0_str.ghn"))
+    np.save(os.path.join(HERE, "index_cfg0_str_X.npy"), w.X)
+
     # the walkthrough scenario (test_explore.py:61-84) as a fixture as well
     X = np.array([[5.4, 5.4], [4.2, 5.5], [6.7, 5.5], [5.5, 6.9], [7.9, 7.9], [9.5, 9.5]])
     run_case(ref, "walkthrough", X, np.array([0, 0, 1, 1, 1, 0]), np.array([[5.5, 5.5]]), 3,
