@@ -95,6 +95,16 @@ typedef struct ghn_fit_out {
 int32_t ghn_fit_build(const ghn_fit_plan *plan, const void *X, const ghn_fit_out *out,
                       void *workspace, size_t workspace_bytes, void *stream);
 
+/* Max-splits width fit (grid.fit_cell_measurements, grid.py:94-109): per
+ * dimension the largest split count s <= min(#distinct, ceil(2 span /
+ * max gap), max_splits) whose s equal bins over [min, max] are all occupied.
+ * X (n, d) device, row-major; widths / splits / origin are HOST arrays of d
+ * (origin = per-dimension minimum).  max_splits <= 0 means no cap. */
+size_t ghn_fit_widths_workspace_size(int64_t n);
+int32_t ghn_fit_widths(const void *X, int32_t dtype, int64_t n, int32_t d, int64_t max_splits,
+                       double *widths, int64_t *splits, double *origin, void *workspace,
+                       size_t workspace_bytes, void *stream);
+
 /* ---------------------------------------------------------------- query
  * Replaces explore.knn_query (explore.py:66-137) with core.ordering_keys /
  * keys_to_distances (core.py:72-91), batched over nq queries, with the

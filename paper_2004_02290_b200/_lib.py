@@ -27,6 +27,8 @@ EXPORTS = (
     "ghn_fit_bounds",
     "ghn_fit_plan_init",
     "ghn_fit_build",
+    "ghn_fit_widths_workspace_size",
+    "ghn_fit_widths",
     "ghn_query_workspace_size",
     "ghn_query_order",
     "ghn_query",
@@ -102,6 +104,10 @@ def lib():
     L.ghn_fit_plan_init.restype = _i32
     L.ghn_fit_build.argtypes = [ctypes.POINTER(FitPlan), _p, ctypes.POINTER(FitOut), _p, _sz, _p]
     L.ghn_fit_build.restype = _i32
+    L.ghn_fit_widths_workspace_size.argtypes = [_i64]
+    L.ghn_fit_widths_workspace_size.restype = _sz
+    L.ghn_fit_widths.argtypes = [_p, _i32, _i64, _i32, _i64, _p, _p, _p, _p, _sz, _p]
+    L.ghn_fit_widths.restype = _i32
     L.ghn_query_workspace_size.argtypes = [ctypes.POINTER(IndexView), _i64, _i32]
     L.ghn_query_workspace_size.restype = _sz
     L.ghn_query.argtypes = [ctypes.POINTER(IndexView), _p, _i32, _i64, _i32, _i32, _i32, _p,

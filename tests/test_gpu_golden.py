@@ -96,3 +96,24 @@ def test_drop_in_build_with_fitted_params(ghn):
     assert list(p.splits) == [7, 8]
     index = ghn.build(ghn.points_from_arrays(X, [0] * 8))
     assert sum(len(b) for b in index.table.values()) == 8
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_fit_widths_match_port_at_scale(ghn, seed):
+    """Device max-splits fit == the pinned numpy port (grid.py:47-109) on larger
+    columns: uniform, clustered, integer-valued (duplicates), fp32, with caps."""
+    from oracle import ghn_port
+
+    rng = np.random.default_rng(900 + seed)
+    n = [2_000, 50_000, 200_000][seed % 3]
+    cols = [rng.uniform(-7, 13, n), rng.normal(0, 3, n) + 40 * rng.integers(0, 3, n),
+            rng.integers(-50, 50, n).astype(float), np.full(n, 2.5)]
+    X = np.stack(cols, axis=1)
+    if seed % 2:
+        X = X.astype(np.float32)
+    cap = [None, 64, 1000][seed % 3]
+    p = ghn.fit_cell_measurements(ghn.points_from_arrays(X, [0] * n), cap)
+    w, origin, splits = ghn_port.fit_widths(X, cap)
+    assert np.array_equal(p.splits, splits)
+    assert np.array_equal(p.widths, w)
+    assert np.array_equal(p.origin, origin)
