@@ -31,7 +31,8 @@ extern "C" {
 enum { GHN_F32 = 0, GHN_F64 = 1 };
 enum { GHN_LAYOUT_DENSE = 0, GHN_LAYOUT_LIST = 1 };
 enum { GHN_MODE_HEURISTIC = 0, GHN_MODE_GUARANTEED = 1 };           /* explore.py:21 */
-enum { GHN_TASK_NONE = 0, GHN_TASK_CLASSIFY = 1, GHN_TASK_REGRESS_MEAN = 2 };
+enum { GHN_TASK_NONE = 0, GHN_TASK_CLASSIFY = 1, GHN_TASK_REGRESS_MEAN = 2, GHN_TASK_REGRESS_MEDIAN = 3 };
+enum { GHN_METRIC_EUCLIDEAN = 0, GHN_METRIC_MANHATTAN = 1, GHN_METRIC_CHEBYSHEV = 2 };   /* core.py:16 */
 enum { GHN_OK = 0, GHN_ERR_VALUE = 1, GHN_ERR_CUDA = 2, GHN_ERR_UNSUPPORTED = 3 };
 
 /* Thread-local description of the last failure on this thread. */
@@ -131,6 +132,7 @@ typedef struct ghn_index_view {
     const double *targets;       /* original point order; regress only */
     const int32_t *labels_perm;  /* labels in CSR slot order (ghn_gather_i32), or NULL */
     int32_t n_labels;            /* label codes lie in [0, n_labels), or 0 if unknown */
+    int32_t metric;              /* GHN_METRIC_*: ordering key and stop bound (core.py:72-91) */
 } ghn_index_view;
 
 typedef struct ghn_query_out {
@@ -138,7 +140,7 @@ typedef struct ghn_query_out {
     int64_t *idx;                /* (nq, k) original point index, or NULL */
     int32_t *label;              /* (nq) CLASSIFY: winning label code, or NULL */
     double *confidence;          /* (nq) CLASSIFY: count / k, or NULL */
-    double *value;               /* (nq) REGRESS_MEAN: mean target, or NULL */
+    double *value;               /* (nq) REGRESS_MEAN / _MEDIAN: the aggregate, or NULL */
     int64_t *stats;              /* (nq, 3) layers_visited, cells_visited, points_scanned, or NULL */
     unsigned long long *totals;  /* [4] += sum layers, cells, points, queries, or NULL */
 } ghn_query_out;

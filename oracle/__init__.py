@@ -25,6 +25,7 @@ _LIB_PATH = os.path.join(_HERE, "libghn_oracle.so")
 _lib = None
 
 DENSE_LIMIT = 1 << 28
+METRIC_CODES = {"euclidean": 0, "manhattan": 1, "chebyshev": 2}
 
 
 def build_oracle(force: bool = False) -> str:
@@ -45,7 +46,7 @@ def _load():
     P = ctypes.c_void_p
     i64, i32 = ctypes.c_int64, ctypes.c_int32
     lib.ghno_sizeof_index.restype = ctypes.c_size_t
-    lib.ghno_build.argtypes = [P, P, i64, i32, P, i64]
+    lib.ghno_build.argtypes = [P, P, i64, i32, P, i64, i32]
     lib.ghno_build.restype = ctypes.c_int
     lib.ghno_free.argtypes = [P]
     lib.ghno_n_cells.argtypes = [P]
@@ -55,8 +56,9 @@ def _load():
     lib.ghno_export.argtypes = [P, P, P, P, P, P]
     lib.ghno_query.argtypes = [P, P, i64, i32, i32, P, P, P, i32]
     lib.ghno_query.restype = ctypes.c_int
-    lib.ghno_classify.argtypes = [P, P, P, i64, i32, P, P]
+    lib.ghno_classify.argtypes = [P, P, P, i64, i32, P, P, i32]
     lib.ghno_regress_mean.argtypes = [P, P, i64, i32, P]
+    lib.ghno_regress_median.argtypes = [P, P, i64, i32, P]
     lib.ghno_key.argtypes = [P, P, ctypes.c_int]
     lib.ghno_key.restype = ctypes.c_double
     lib.ghno_pairwise_sum.argtypes = [P, i64]
@@ -72,7 +74,7 @@ def _ptr(a: np.ndarray):
 class COracle:
     """Index + batched query through the C restatement."""
 
-    def __init__(self, X, widths, dense_limit: int = DENSE_LIMIT):
+    def __init__(self, X, widths, dense_limit: int = DENSE_LIMIT, metric: str = "euclidean"):
         lib = _load()
         self._lib = lib
         self.X = np.ascontiguousarray(np.asarray(X, dtype=np.float64))
@@ -81,7 +83,9 @@ class COracle:
         self.n, self.d = self.X.shape
         self.widths = np.ascontiguousarray(np.asarray(widths, dtype=np.float64))
         self._ix = ctypes.create_string_buffer(lib.ghno_sizeof_index())
-        rc = lib.ghno_build(self._ix, _ptr(self.X), self.n, self.d, _ptr(self.widths), dense_limit)
+        self.metric = metric
+        rc = lib.ghno_build(self._ix, _ptr(self.X), self.n, self.d, _ptr(self.widths), dense_limit,
+                            METRIC_CODES[metric])
         if rc == 1:
             raise ValueError("non-finite coordinate")
         if rc != 0:
@@ -120,7 +124,7 @@ class COracle:
         return keys, idx, stats
 
 
-def classify(keys, idx, label_codes):
+def classify(keys, idx, label_codes, metric: str = "euclidean"):
     """Vote over int64 label codes per point -> (label code, confidence)."""
     lib = _load()
     keys = np.ascontiguousarray(keys, dtype=np.float64)
@@ -129,7 +133,8 @@ def classify(keys, idx, label_codes):
     nq, k = keys.shape
     out_l = np.empty(nq, np.int64)
     out_c = np.empty(nq, np.float64)
-    lib.ghno_classify(_ptr(keys), _ptr(idx), _ptr(codes), nq, k, _ptr(out_l), _ptr(out_c))
+    lib.ghno_classify(_ptr(keys), _ptr(idx), _ptr(codes), nq, k, _ptr(out_l), _ptr(out_c),
+                      METRIC_CODES[metric])
     return out_l, out_c
 
 
@@ -140,6 +145,16 @@ def regress_mean(idx, targets):
     nq, k = idx.shape
     out = np.empty(nq, np.float64)
     lib.ghno_regress_mean(_ptr(idx), _ptr(t), nq, k, _ptr(out))
+    return out
+
+
+def regress_median(idx, targets):
+    lib = _load()
+    idx = np.ascontiguousarray(idx, dtype=np.int64)
+    t = np.ascontiguousarray(targets, dtype=np.float64)
+    nq, k = idx.shape
+    out = np.empty(nq, np.float64)
+    lib.ghno_regress_median(_ptr(idx), _ptr(t), nq, k, _ptr(out))
     return out
 
 

@@ -77,7 +77,8 @@ def cell_ids(X, widths):
 class PortIndex:
     """Array form of GridIndex (grid.py:128-162): order/starts instead of bucket lists."""
 
-    def __init__(self, X, labels, widths):
+    def __init__(self, X, labels, widths, metric="euclidean"):
+        self.metric = metric
         X = np.asarray(X, dtype=np.float64)
         if X.ndim != 2 or X.shape[0] == 0:
             raise ValueError("X must be a non-empty (n, d) matrix")
@@ -105,6 +106,7 @@ class PortIndex:
         class's lexsort build.  Lets bench.py time knn() at 100M points without
         a 200 s lexsort."""
         self = cls.__new__(cls)
+        self.metric = "euclidean"
         self.X = np.asarray(X, dtype=np.float64)
         self.labels = np.asarray(labels)
         self.widths = np.asarray(widths, dtype=np.float64)
@@ -127,15 +129,19 @@ class PortIndex:
         return self.order[self.starts[c]:self.ends[c]]
 
 
-def build(X, labels, widths):
-    return PortIndex(X, labels, widths)
+def build(X, labels, widths, metric="euclidean"):
+    return PortIndex(X, labels, widths, metric)
 
 
 # ---------------------------------------------------------------------- query
-def ordering_keys(q, pts):
-    """Squared L2 in numpy einsum order (core.py:78-80)."""
+def ordering_keys(q, pts, metric="euclidean"):
+    """Per-row keys (core.py:72-86): squared L2 in einsum order, L1, L-inf."""
     diff = pts - q
-    return np.einsum("ij,ij->i", diff, diff)
+    if metric == "euclidean":
+        return np.einsum("ij,ij->i", diff, diff)
+    if metric == "manhattan":
+        return np.abs(diff).sum(axis=1)
+    return np.abs(diff).max(axis=1)
 
 
 def knn(index: PortIndex, q, k, mode="heuristic"):
@@ -160,7 +166,7 @@ def knn(index: PortIndex, q, k, mode="heuristic"):
         moved = False
         if hit.size:
             cand = np.concatenate([index.bucket(c) for c in hit])
-            ck = ordering_keys(q, index.X[cand])
+            ck = ordering_keys(q, index.X[cand], index.metric)
             n_cells += hit.size
             n_pts += cand.size
             mk = np.concatenate([keys, ck])
@@ -173,7 +179,7 @@ def knn(index: PortIndex, q, k, mode="heuristic"):
                 break
             if mode == "guaranteed":
                 b = layer * wmin
-                if b * b > keys[-1]:
+                if (b * b if index.metric == "euclidean" else b) > keys[-1]:
                     break
         if layer >= last:
             break
@@ -182,7 +188,7 @@ def knn(index: PortIndex, q, k, mode="heuristic"):
 
 
 # ------------------------------------------------------------------ epilogues
-def classify(keys, idx, labels):
+def classify(keys, idx, labels, metric="euclidean"):
     """Majority vote; ties -> label of min (sqrt key, index) (predict.py:20-36)."""
     labs = [labels[i] for i in idx]
     tally = Counter(labs)
@@ -191,7 +197,7 @@ def classify(keys, idx, labels):
     if len(tied) == 1:
         (win,) = tied
     else:
-        dist = np.sqrt(keys)
+        dist = np.sqrt(keys) if metric == "euclidean" else keys
         win = min(
             ((float(dist[a]), int(idx[a]), labs[a]) for a in range(len(labs)) if labs[a] in tied),
             key=lambda t: (t[0], t[1]),

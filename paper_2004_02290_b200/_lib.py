@@ -17,7 +17,8 @@ GHN_MAX_DIM = 16
 GHN_F32, GHN_F64 = 0, 1
 GHN_LAYOUT_DENSE, GHN_LAYOUT_LIST = 0, 1
 GHN_MODE = {"heuristic": 0, "guaranteed": 1}
-GHN_TASK_NONE, GHN_TASK_CLASSIFY, GHN_TASK_REGRESS_MEAN = 0, 1, 2
+GHN_TASK_NONE, GHN_TASK_CLASSIFY, GHN_TASK_REGRESS_MEAN, GHN_TASK_REGRESS_MEDIAN = 0, 1, 2, 3
+GHN_METRIC = {"euclidean": 0, "manhattan": 1, "chebyshev": 2}
 GHN_OK, GHN_ERR_VALUE, GHN_ERR_CUDA, GHN_ERR_UNSUPPORTED = 0, 1, 2, 3
 
 # Every symbol include/ghn.h declares (checked by tests/test_abi.py).
@@ -69,7 +70,7 @@ class IndexView(ctypes.Structure):
         ("ext", _i64 * GHN_MAX_DIM),
         ("coords", _p), ("perm", _p), ("cell_start", _p), ("cell_ids", _p),
         ("pt_off", _p), ("ne_off", _p), ("labels", _p), ("targets", _p), ("labels_perm", _p),
-        ("n_labels", _i32),
+        ("n_labels", _i32), ("metric", _i32),
     ]
 
 

@@ -81,6 +81,54 @@ __device__ __forceinline__ double key_numpy_order_rt(const double *diff, int d) 
     return __dadd_rn(a0, a1);
 }
 
+// numpy pairwise summation (add.reduce over a contiguous row) of |diff|:
+// the manhattan key np.abs(diff).sum(axis=1) (core.py:81-82).  d <= 16.
+__device__ __forceinline__ double pairwise_abs_sum(const double *v, int n) {
+    if (n < 8) {
+        double r = fabs(v[0]);
+        for (int i = 1; i < n; ++i) r = __dadd_rn(r, fabs(v[i]));
+        return r;
+    }
+    double acc[8];
+    for (int t = 0; t < 8; ++t) acc[t] = fabs(v[t]);
+    int i = 8;
+    for (; i < n - (n % 8); i += 8)
+        for (int t = 0; t < 8; ++t) acc[t] = __dadd_rn(acc[t], fabs(v[i + t]));
+    double r = __dadd_rn(__dadd_rn(__dadd_rn(acc[0], acc[1]), __dadd_rn(acc[2], acc[3])),
+                         __dadd_rn(__dadd_rn(acc[4], acc[5]), __dadd_rn(acc[6], acc[7])));
+    for (; i < n; ++i) r = __dadd_rn(r, fabs(v[i]));
+    return r;
+}
+
+// Ordering key of a difference vector for a metric (core.py:72-86).
+template <int D>
+__device__ __forceinline__ double metric_key(const double (&diff)[D], int metric) {
+    if (metric == GHN_METRIC_EUCLIDEAN) return key_numpy_order<D>(diff);
+    if (metric == GHN_METRIC_MANHATTAN) return pairwise_abs_sum(diff, D);
+    double m = fabs(diff[0]);
+#pragma unroll
+    for (int j = 1; j < D; ++j) m = fmax(m, fabs(diff[j]));
+    return m;
+}
+
+__device__ __forceinline__ double metric_key_rt(const double *diff, int d, int metric) {
+    if (metric == GHN_METRIC_EUCLIDEAN) return key_numpy_order_rt(diff, d);
+    if (metric == GHN_METRIC_MANHATTAN) return pairwise_abs_sum(diff, d);
+    double m = fabs(diff[0]);
+    for (int j = 1; j < d; ++j) m = fmax(m, fabs(diff[j]));
+    return m;
+}
+
+// Guaranteed-stop bound key for layer l (explore.py:124-125) and the
+// reported distance of a key (core.py:89-91).
+__device__ __forceinline__ double bound_key(int64_t l, double min_w, int metric) {
+    const double b = __dmul_rn((double)l, min_w);
+    return metric == GHN_METRIC_EUCLIDEAN ? __dmul_rn(b, b) : b;
+}
+__device__ __forceinline__ double key_to_dist(double key, int metric) {
+    return metric == GHN_METRIC_EUCLIDEAN ? sqrt(key) : key;
+}
+
 // (key, index) lexicographic order (explore.py:114).
 __device__ __forceinline__ bool pair_less(double ka, int32_t ia, double kb, int32_t ib) {
     return ka < kb || (ka == kb && ia < ib);

@@ -170,11 +170,11 @@ __device__ __forceinline__ void consume(const QArgs &a, const double *qd, int d,
 #pragma unroll
                 for (int j = 0; j < DC; ++j)
                     df[j] = __dsub_rn(to_double(coords[(int64_t)j * n + slot]), qd[j]);
-                key = key_numpy_order<DC>(df);
+                key = metric_key<DC>(df, a.ix.metric);
             } else {
                 double df[GHN_MAX_DIM];
                 for (int j = 0; j < d; ++j) df[j] = __dsub_rn(to_double(coords[(int64_t)j * n + slot]), qd[j]);
-                key = key_numpy_order_rt(df, d);
+                key = metric_key_rt(df, d, a.ix.metric);
             }
         }
         bool pass = act && (tk.filled < k || key <= tk.thr_key);
@@ -378,8 +378,7 @@ __device__ __forceinline__ void query_one(const QArgs &a, int64_t w) {
         if (full) {
             if (a.mode == GHN_MODE_HEURISTIC && !acc.changed) break;
             if (a.mode == GHN_MODE_GUARANTEED) {
-                const double b = __dmul_rn((double)l, ix.min_width);
-                if (__dmul_rn(b, b) > tk.thr_key) break;
+                if (bound_key(l, ix.min_width, ix.metric) > tk.thr_key) break;
             }
         }
         if (l >= lmax) break;
@@ -394,19 +393,18 @@ __device__ __forceinline__ void query_one(const QArgs &a, int64_t w) {
                     l = next;
                     continue;
                 }
-                // guaranteed: smallest l' in (l, next) with (l' * min_w)^2 > kth
-                const double est = floor(sqrt(tk.thr_key) / ix.min_width) - 2.0;
+                // guaranteed: smallest l' in (l, next) with bound(l') > kth
+                const double est =
+                    floor((ix.metric == GHN_METRIC_EUCLIDEAN ? sqrt(tk.thr_key) : tk.thr_key) / ix.min_width) - 2.0;
                 int64_t lp = l + 1;
                 if (est > (double)lp && est < (double)next) lp = (int64_t)est;
                 while (lp > l + 1) {
-                    const double b = __dmul_rn((double)(lp - 1), ix.min_width);
-                    if (__dmul_rn(b, b) > tk.thr_key) --lp;
+                    if (bound_key(lp - 1, ix.min_width, ix.metric) > tk.thr_key) --lp;
                     else break;
                 }
                 bool stop = false;
                 for (; lp < next; ++lp) {
-                    const double b = __dmul_rn((double)lp, ix.min_width);
-                    if (__dmul_rn(b, b) > tk.thr_key) {
+                    if (bound_key(lp, ix.min_width, ix.metric) > tk.thr_key) {
                         stop = true;
                         break;
                     }
@@ -429,7 +427,7 @@ __device__ __forceinline__ void query_one(const QArgs &a, int64_t w) {
             const int t = s * 32 + lane;
             if (t < k) {
                 if (o.idx) o.idx[qi * k + t] = tk.idx[s];
-                if (o.dist) o.dist[qi * k + t] = sqrt(tk.key[s]);
+                if (o.dist) o.dist[qi * k + t] = key_to_dist(tk.key[s], ix.metric);
             }
         }
     }
@@ -479,7 +477,7 @@ __device__ __forceinline__ void query_one(const QArgs &a, int64_t w) {
 #pragma unroll
         for (int s = 0; s < KS; ++s) {
             if (s * 32 + lane < k && cnt[s] == top) {
-                const double dd = sqrt(tk.key[s]);
+                const double dd = key_to_dist(tk.key[s], ix.metric);
                 if (pair_less(dd, tk.idx[s], bd, bi)) {
                     bd = dd;
                     bi = tk.idx[s];
@@ -511,6 +509,52 @@ __device__ __forceinline__ void query_one(const QArgs &a, int64_t w) {
         }
         const double mean = pairwise_mean<KS>(v, k);
         if (lane == 0 && o.value) o.value[qi] = mean;
+    } else if (a.task == GHN_TASK_REGRESS_MEDIAN && ix.targets) {
+        // np.median (predict.py:46-47): the middle order statistic, or the
+        // mean (a + b) / 2 of the two middle ones for even k
+        double v[KS];
+        int rank[KS];
+#pragma unroll
+        for (int s = 0; s < KS; ++s) {
+            const int t = s * 32 + lane;
+            v[s] = t < k ? ix.targets[tk.idx[s]] : INFINITY;
+            rank[s] = 0;
+        }
+#pragma unroll
+        for (int s2 = 0; s2 < KS; ++s2) {
+            if (s2 * 32 >= k) break;
+            for (int src = 0; src < 32; ++src) {
+                const int t2 = s2 * 32 + src;
+                if (t2 >= k) break;
+                const double x = shfl_d(v[s2], src);
+#pragma unroll
+                for (int s = 0; s < KS; ++s) {
+                    const int t = s * 32 + lane;
+                    rank[s] += (x < v[s] || (x == v[s] && t2 < t)) ? 1 : 0;
+                }
+            }
+        }
+        const int r1 = (k - 1) / 2, r2 = k / 2;
+        double m1 = 0.0, m2 = 0.0;
+        bool h1 = false, h2 = false;
+#pragma unroll
+        for (int s = 0; s < KS; ++s) {
+            if (s * 32 + lane < k) {
+                if (rank[s] == r1) {
+                    m1 = v[s];
+                    h1 = true;
+                }
+                if (rank[s] == r2) {
+                    m2 = v[s];
+                    h2 = true;
+                }
+            }
+        }
+        const unsigned b1 = __ballot_sync(GHN_FULL, h1), b2 = __ballot_sync(GHN_FULL, h2);
+        m1 = shfl_d(m1, __ffs(b1) - 1);
+        m2 = shfl_d(m2, __ffs(b2) - 1);
+        const double med = (k & 1) ? m1 : __ddiv_rn(__dadd_rn(m1, m2), 2.0);
+        if (lane == 0 && o.value) o.value[qi] = med;
     }
 }
 

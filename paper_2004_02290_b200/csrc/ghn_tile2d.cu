@@ -932,6 +932,7 @@ bool tile2d_plan(const ghn_index_view *ix, int64_t nq, int32_t k, int32_t task, 
     memset(plan, 0, sizeof(*plan));
     if (ix->layout != GHN_LAYOUT_DENSE || ix->d != 2 || ix->dtype != GHN_F32) return false;
     if (task != GHN_TASK_CLASSIFY || want_neighbors || !ix->labels_perm) return false;
+    if (ix->metric != GHN_METRIC_EUCLIDEAN) return false;
     if (nq < 4096 || k < 1 || k > 256) return false;
     const double rho = (double)ix->n / (double)ix->E;      // points per bbox cell
     int lf = 0;

@@ -108,7 +108,7 @@ def _run(index: GridIndex, Qt, k, mode, task, want_neighbors, want_stats, want_t
         if want_confidence:
             res["confidence"] = torch.empty(nq, dtype=torch.float64, device=dev)
             out.confidence = _lib.ptr(res["confidence"])
-    elif task == _lib.GHN_TASK_REGRESS_MEAN:
+    elif task in (_lib.GHN_TASK_REGRESS_MEAN, _lib.GHN_TASK_REGRESS_MEDIAN):
         if index._labels.targets is None:
             raise ValueError("labels are not numeric targets")
         res["value"] = torch.empty(nq, dtype=torch.float64, device=dev)

@@ -249,6 +249,7 @@ class GridIndex:
         v.targets = _lib.ptr(self._labels.targets)
         v.labels_perm = _lib.ptr(self.labels_perm)
         v.n_labels = self._labels.n_codes
+        v.metric = _lib.GHN_METRIC[self.metric]
         return v
 
 

@@ -55,7 +55,8 @@ def regress(neighbors: Sequence[Neighbor], agg: str = "mean") -> Prediction:
     raise ValueError(f"unknown aggregation {agg!r}; expected 'mean' or 'median'")
 
 
-TASKS = {"classify": _lib.GHN_TASK_CLASSIFY, "regress": _lib.GHN_TASK_REGRESS_MEAN}
+TASKS = {"classify": _lib.GHN_TASK_CLASSIFY, "regress": _lib.GHN_TASK_REGRESS_MEAN,
+         "regress_median": _lib.GHN_TASK_REGRESS_MEDIAN}
 
 
 def predict_batch(index: GridIndex, Q, k: int, mode: str = "heuristic", task: str = "classify",
@@ -65,7 +66,8 @@ def predict_batch(index: GridIndex, Q, k: int, mode: str = "heuristic", task: st
 
     Returns a dict of device tensors: task "classify" -> ``label`` (int32
     label codes; ``index.decode_labels`` maps them back) and ``confidence``;
-    task "regress" -> ``value`` (fp64 mean).  Optional ``dist``/``idx``
+    task "regress" -> ``value`` (fp64 mean), "regress_median" -> ``value``
+    (np.median of the k targets).  Optional ``dist``/``idx``
     (neighbours), ``stats`` (nq, 3) and ``totals`` (sum layers, cells,
     points, queries).  ``qorder``: a visit order from ``query_order`` (else
     queries are binned internally).

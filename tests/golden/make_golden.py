@@ -39,16 +39,17 @@ def load_reference():
     return mod
 
 
-def run_case(ref, name, X, y, Q, k, mode, task, widths=None, max_splits=None, notes=""):
+def run_case(ref, name, X, y, Q, k, mode, task, widths=None, max_splits=None, notes="", metric="euclidean",
+             agg="mean"):
     """Run the reference on (X, y) and queries Q; save everything."""
     Xf = np.asarray(X, dtype=np.float64)           # the reference upcasts (core.py:32)
     pts = ref.points_from_arrays(Xf, list(y.tolist()))
     if widths is None:
-        index = ref.build(pts, max_splits=max_splits)
+        index = ref.build(pts, metric=metric, max_splits=max_splits)
     else:
         d = Xf.shape[1]
         params = ref.GridParams(np.asarray(widths, dtype=np.float64), Xf.min(axis=0), np.ones(d, np.int64))
-        index = ref.build(pts, params=params)
+        index = ref.build(pts, metric=metric, params=params)
     order = np.concatenate(index.buckets).astype(np.int64)
     sizes = np.array([b.size for b in index.buckets], np.int64)
     nq = Q.shape[0]
@@ -67,7 +68,7 @@ def run_case(ref, name, X, y, Q, k, mode, task, widths=None, max_splits=None, no
             pred[i] = p.value
             conf[i] = p.confidence
         else:
-            p = ref.regress(nbrs, "mean")
+            p = ref.regress(nbrs, agg)
             pred[i] = p.value
             conf[i] = np.nan
     np.savez_compressed(
@@ -81,7 +82,7 @@ def run_case(ref, name, X, y, Q, k, mode, task, widths=None, max_splits=None, no
         order=order, bucket_sizes=sizes,
         cell_array=np.asarray(index.cell_array, np.int64),
         nb_idx=nb_idx, nb_dist=nb_dist, stats=stats, pred=pred, conf=conf,
-        notes=np.array(notes))
+        notes=np.array(notes), metric=np.array(metric), agg=np.array(agg))
     print(f"case_{name}: n={X.shape[0]} d={X.shape[1]} nq={nq} k={k} mode={mode} "
           f"cells={sizes.size} mean_layers={stats[:, 0].mean():.2f} mean_points={stats[:, 2].mean():.1f}")
 
@@ -156,6 +157,22 @@ def main():
         yy = y.astype(np.float64) * 1.25 - 0.5 if task == "regress" else y
         ms = 7 if t % 7 == 6 else None
         run_case(ref, f"fit{t:02d}", X, yy, Q, k, mode, task, max_splits=ms)
+
+    # other metrics (core.py:81-84, explore.py:125) and the median (predict.py:46-47)
+    for mt in ("manhattan", "chebyshev"):
+        w = datagen.cfg1(n=8000, nq=120, seed=110)
+        run_case(ref, f"metric_{mt}_heur", w.X, w.y, w.Q, 7, "heuristic", "classify", widths=w.widths,
+                 metric=mt)
+        run_case(ref, f"metric_{mt}_guar", w.X, w.y, w.Q[:60], 7, "guaranteed", "classify",
+                 widths=w.widths, metric=mt)
+    rng2 = np.random.default_rng(111)
+    X = rng2.normal(0, 2, (900, 5))
+    y = np.round(rng2.normal(0, 3, 900), 1)
+    Q = X[rng2.integers(0, 900, 40)] + rng2.normal(0, 0.4, (40, 5))
+    run_case(ref, "metric_manhattan_fit5", X, y, Q, 9, "guaranteed", "regress", metric="manhattan")
+    w = datagen.cfg2(n=5000, nq=50, seed=112)
+    run_case(ref, "median_even_k", w.X, w.y, w.Q, 16, "heuristic", "regress", widths=w.widths, agg="median")
+    run_case(ref, "median_odd_k", w.X, w.y, w.Q, 9, "heuristic", "regress", widths=w.widths, agg="median")
 
     # index files written by the reference's save_index (grid.py:211-246)
     rng = np.random.default_rng(515)

@@ -25,7 +25,7 @@ def ghn():
 def test_build_matches_reference(ghn, name):
     c = load_case(name)
     params = ghn.GridParams(c["widths"], c["origin"], c["splits"])
-    ix = ghn.build_arrays(c["X"], c["y"], params=params)
+    ix = ghn.build_arrays(c["X"], c["y"], params=params, metric=str(c["metric"]))
     assert ix.n_cells == c["bucket_sizes"].size
     assert np.array_equal(ix.order, c["order"])
     assert np.array_equal(ix.cell_array, c["cell_array"])
@@ -36,7 +36,7 @@ def test_build_matches_reference(ghn, name):
 def test_knn_matches_reference(ghn, name):
     c = load_case(name)
     params = ghn.GridParams(c["widths"], c["origin"], c["splits"])
-    ix = ghn.build_arrays(c["X"], c["y"], params=params)
+    ix = ghn.build_arrays(c["X"], c["y"], params=params, metric=str(c["metric"]))
     k, mode = int(c["k"]), str(c["mode"])
     dist, idx, stats = ghn.knn_query_batch(ix, c["Q"], k, mode)
     assert np.array_equal(idx.cpu().numpy(), c["nb_idx"])
@@ -50,7 +50,9 @@ def test_fused_epilogue_matches_reference(ghn, name):
     params = ghn.GridParams(c["widths"], c["origin"], c["splits"])
     task = str(c["task"])
     y = c["y"]
-    ix = ghn.build_arrays(c["X"], y, params=params)
+    ix = ghn.build_arrays(c["X"], y, params=params, metric=str(c["metric"]))
+    if task == "regress" and str(c["agg"]) == "median":
+        task = "regress_median"
     r = ghn.predict_batch(ix, c["Q"], int(c["k"]), str(c["mode"]), task=task)
     if task == "classify":
         labels = np.asarray(ghn.decode_labels(ix, r["label"]), dtype=np.float64)

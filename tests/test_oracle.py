@@ -37,11 +37,15 @@ def test_pairwise_mean_matches_fixture():
         assert oracle.pairwise_sum(t) / k == z[f"mean{k}"], k
 
 
+def _dist(keys, c):
+    return np.sqrt(keys) if str(c["metric"]) == "euclidean" else keys
+
+
 @pytest.mark.parametrize("name", CASES)
 def test_c_oracle_matches_reference(name):
     c = load_case(name)
     X = c["X"].astype(np.float64)
-    ix = oracle.COracle(X, c["widths"])
+    ix = oracle.COracle(X, c["widths"], metric=str(c["metric"]))
     order, cids, starts, lo, ext = ix.export()
     assert np.array_equal(order, c["order"])
     assert np.array_equal(cids, c["cell_array"])
@@ -49,13 +53,15 @@ def test_c_oracle_matches_reference(name):
     k = int(c["k"])
     keys, idx, stats = ix.query(c["Q"], k, str(c["mode"]), threads=2)
     assert np.array_equal(idx, c["nb_idx"])
-    assert np.array_equal(np.sqrt(keys), c["nb_dist"])
+    assert np.array_equal(_dist(keys, c), c["nb_dist"])
     assert np.array_equal(stats, c["stats"])
     if str(c["task"]) == "classify":
         codes = c["y"].astype(np.int64)
-        lab, conf = oracle.classify(keys, idx, codes)
+        lab, conf = oracle.classify(keys, idx, codes, str(c["metric"]))
         assert np.array_equal(lab.astype(np.float64), c["pred"])
         assert np.array_equal(conf, c["conf"])
+    elif str(c["agg"]) == "median":
+        assert np.array_equal(oracle.regress_median(idx, c["y"].astype(np.float64)), c["pred"])
     else:
         val = oracle.regress_mean(idx, c["y"].astype(np.float64))
         assert np.array_equal(val, c["pred"])
@@ -65,7 +71,7 @@ def test_c_oracle_matches_reference(name):
 def test_c_oracle_list_mode_matches_reference(name):
     """Force the cell-list scan (dense_limit=0): the explore.py:105 restatement."""
     c = load_case(name)
-    ix = oracle.COracle(c["X"].astype(np.float64), c["widths"], dense_limit=0)
+    ix = oracle.COracle(c["X"].astype(np.float64), c["widths"], dense_limit=0, metric=str(c["metric"]))
     order, cids, starts, _, _ = ix.export()
     assert np.array_equal(order, c["order"])
     assert np.array_equal(cids, c["cell_array"])
@@ -77,20 +83,20 @@ def test_c_oracle_list_mode_matches_reference(name):
 @pytest.mark.parametrize("name", [n for n in CASES if not n.startswith("fit")] + ["fit03", "fit07"])
 def test_numpy_port_matches_reference(name):
     c = load_case(name)
-    ix = ghn_port.build(c["X"], c["y"], c["widths"])
+    ix = ghn_port.build(c["X"], c["y"], c["widths"], str(c["metric"]))
     assert np.array_equal(ix.order, c["order"])
     assert np.array_equal(ix.cell_array, c["cell_array"])
     k = int(c["k"])
     for qi in range(min(40, c["Q"].shape[0])):
         keys, idx, st = ghn_port.knn(ix, c["Q"][qi], k, str(c["mode"]))
         assert np.array_equal(idx, c["nb_idx"][qi])
-        assert np.array_equal(np.sqrt(keys), c["nb_dist"][qi])
+        assert np.array_equal(_dist(keys, c), c["nb_dist"][qi])
         assert list(st) == list(c["stats"][qi])
         if str(c["task"]) == "classify":
-            lab, conf = ghn_port.classify(keys, idx, c["y"])
+            lab, conf = ghn_port.classify(keys, idx, c["y"], str(c["metric"]))
             assert lab == c["pred"][qi] and conf == c["conf"][qi]
         else:
-            assert ghn_port.regress(idx, c["y"]) == c["pred"][qi]
+            assert ghn_port.regress(idx, c["y"], str(c["agg"])) == c["pred"][qi]
 
 
 @pytest.mark.parametrize("name", [n for n in CASES if n.startswith("fit")])
