@@ -38,6 +38,9 @@ constexpr int T2_NB = 32;        // histogram buckets per select round
 constexpr int T2_SMALL = 4;      // boundary candidates ordered exactly
 constexpr int T2_NL = 4;         // distinct labels tracked by the vote
 constexpr int T2_CAP = 4096;     // staged points per tile
+#ifndef T2_MINB
+#define T2_MINB 4
+#endif
 
 struct T2Args {
     int64_t n;
@@ -56,7 +59,7 @@ struct T2Args {
     int32_t mode;
     const int32_t *qorder;
     const int32_t *tile_start;
-    int32_t T, A, nt0, nt1, win;
+    int32_t T, A, nt0, nt1, win, cap;
     int32_t *out_label;
     double *out_conf;
     int64_t *out_stats;
@@ -753,7 +756,7 @@ __device__ __forceinline__ void process_query_w(const T2Args &a, const Win &w, W
     }
 }
 
-__global__ void __launch_bounds__(T2_THREADS) tile2d_kernel(const T2Args a) {
+__global__ void __launch_bounds__(T2_THREADS, T2_MINB) tile2d_kernel(const T2Args a) {
     extern __shared__ __align__(16) unsigned char sm[];
     __shared__ int s_P;
     __shared__ WarpScratch s_scratch[T2_THREADS / 32];
@@ -765,8 +768,8 @@ __global__ void __launch_bounds__(T2_THREADS) tile2d_kernel(const T2Args a) {
     const int c_lo = max(t1 * a.T - a.A, 0), c_hi = min(t1 * a.T + a.T - 1 + a.A, a.ext1 - 1);
     const int R = r_hi - r_lo + 1, W = c_hi - c_lo + 1, W1 = W + 1;
     float *sx = (float *)sm;
-    float *sy = sx + T2_CAP;
-    int32_t *loc = (int32_t *)(sy + T2_CAP);                       // [R][W+1]
+    float *sy = sx + a.cap;
+    int32_t *loc = (int32_t *)(sy + a.cap);                        // [R][W+1]
     int32_t *delta = loc + a.win * (a.win + 1);                    // [R]
     int32_t *rstart = delta + a.win;                               // [R+1]
     for (int e = threadIdx.x; e < R * W1; e += blockDim.x) {
@@ -793,7 +796,7 @@ __global__ void __launch_bounds__(T2_THREADS) tile2d_kernel(const T2Args a) {
     }
     __syncthreads();
     const int P = s_P;
-    if (P > T2_CAP) {
+    if (P > a.cap) {
         for (int qq = qb + threadIdx.x; qq < qe; qq += blockDim.x) push_fallback(a, a.qorder[qq]);
         return;
     }
@@ -834,8 +837,8 @@ __global__ void __launch_bounds__(T2_THREADS) tile2d_grp_kernel(const T2Args a) 
     const int c_lo = max(t1 * a.T - a.A, 0), c_hi = min(t1 * a.T + a.T - 1 + a.A, a.ext1 - 1);
     const int R = r_hi - r_lo + 1, W = c_hi - c_lo + 1, W1 = W + 1;
     float *sx = (float *)sm;
-    float *sy = sx + T2_CAP;
-    int32_t *loc = (int32_t *)(sy + T2_CAP);                       // [R][W+1]
+    float *sy = sx + a.cap;
+    int32_t *loc = (int32_t *)(sy + a.cap);                        // [R][W+1]
     int32_t *delta = loc + a.win * (a.win + 1);                    // [R]
     int32_t *rstart = delta + a.win;                               // [R+1]
     for (int e = threadIdx.x; e < R * W1; e += blockDim.x) {
@@ -862,7 +865,7 @@ __global__ void __launch_bounds__(T2_THREADS) tile2d_grp_kernel(const T2Args a) 
     }
     __syncthreads();
     const int P = s_P;
-    if (P > T2_CAP) {
+    if (P > a.cap) {
         for (int qq = qb + threadIdx.x; qq < qe; qq += blockDim.x) push_fallback(a, a.qorder[qq]);
         return;
     }
@@ -956,7 +959,15 @@ bool tile2d_plan(const ghn_index_view *ix, int64_t nq, int32_t k, int32_t task, 
     plan->G = 32;
     if (k == 1 && ix->n_labels > 0 && ix->n_labels <= 32) plan->G = 8;
     if (getenv("GHN_TILE_G")) plan->G = atoi(getenv("GHN_TILE_G"));
-    plan->smem = (size_t)T2_CAP * 8 +
+    // staged-point capacity: the expected window plus margin (an overflowing
+    // tile sends its queries to the generic kernel)
+    const double expect = (double)plan->win * plan->win * rho;
+    int cap = (int)(1.2 * expect + 128.0);
+    cap = (cap + 127) & ~127;
+    if (cap > 8192) cap = 8192;
+    if (cap < 256) cap = 256;
+    plan->cap = cap;
+    plan->smem = (size_t)cap * 8 +
                  (size_t)plan->win * (plan->win + 1) * 4 + (size_t)plan->win * 4 +
                  (size_t)(plan->win + 1) * 4 + 64;
     if (plan->smem > 200 * 1024) return false;
@@ -1025,6 +1036,7 @@ int32_t tile2d_run(const ghn_index_view *ix, const Tile2dPlan *plan, const void 
     a.nt0 = plan->nt0;
     a.nt1 = plan->nt1;
     a.win = plan->win;
+    a.cap = plan->cap;
     a.out_label = out->label;
     a.out_conf = out->confidence;
     a.out_stats = out->stats;

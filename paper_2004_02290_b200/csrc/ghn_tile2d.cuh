@@ -12,6 +12,7 @@ struct Tile2dPlan {
     int64_t ntiles;
     int32_t win;      // T + 2A
     int32_t G;        // lanes per query (32: warp kernel; 8/16: group kernel)
+    int32_t cap;      // staged points per CTA
     size_t smem;      // dynamic shared memory per CTA
 };
 
