@@ -316,7 +316,7 @@ def run_ours(args):
     # ---- algorithmic bytes per k (untimed, deterministic): S_q from the device counters
     scanned = {}
     for k in ks:
-        r = predict_batch(index, Q_d, k, totals=True, confidence=False)
+        r = predict_batch(index, Q_d, k, task=w.task, totals=True, confidence=False)
         tot = r["totals"].cpu().numpy()
         scanned[k] = {"layers": int(tot[0]), "cells": int(tot[1]), "points": int(tot[2])}
     algo_bytes = {k: 4 * d * (nq + scanned[k]["points"]) + 4 * nq for k in ks}
@@ -327,7 +327,7 @@ def run_ours(args):
         for k in ks:
             e0, e1 = (torch.cuda.Event(enable_timing=True) for _ in range(2))
             e0.record(stream)
-            predict_batch(index, Q_d, k, confidence=False)
+            predict_batch(index, Q_d, k, task=w.task, confidence=False)
             e1.record(stream)
             ev.append((k, e0, e1))
         return ev
@@ -367,12 +367,13 @@ def run_ours(args):
     e2e = None
     if not args.no_e2e:
         Q_h = torch.from_numpy(w.Q).pin_memory()
-        lab_h = torch.empty(nq, dtype=torch.int32).pin_memory()
+        out_key = "label" if w.task == "classify" else "value"
+        lab_h = torch.empty(nq, dtype=torch.int32 if w.task == "classify" else torch.float64).pin_memory()
         def e2e_step():
             for k in ks:
                 Qd = Q_h.to(dev, non_blocking=True)
-                r = predict_batch(index, Qd, k, confidence=False)
-                lab_h.copy_(r["label"], non_blocking=True)
+                r = predict_batch(index, Qd, k, task=w.task, confidence=False)
+                lab_h.copy_(r[out_key], non_blocking=True)
         e2e_step()
         torch.cuda.synchronize()
         e2e_ms = 0.0
@@ -389,7 +390,7 @@ def run_ours(args):
         e2e_ms = max_over_ranks(e2e_ms / args.steps, world)
         e2e = {"value": world * queries_per_step / (e2e_ms / 1e3), "unit": "queries/s",
                "h2d_bytes_per_step": len(ks) * int(Q_h.numel() * 4),
-               "d2h_bytes_per_step": len(ks) * int(lab_h.numel() * 4), "ms_per_step": e2e_ms}
+               "d2h_bytes_per_step": len(ks) * int(lab_h.numel() * lab_h.element_size()), "ms_per_step": e2e_ms}
 
     # ---- CPU legs (rank 0, N=1 only)
     cpu_baseline = None
@@ -418,7 +419,7 @@ def run_ours(args):
             "warmup": args.warmup, "ms_per_step": step_ms_max, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"cfg{cfg}: {n} x {d}-D uniform fp32, {nq} queries/rank, "
-                                   f"C={w.cells_per_axis}, k sweep {ks}, heuristic stop, vote",
+                                   f"C={w.cells_per_axis}, k sweep {ks}, heuristic stop, {w.task}",
                        "n_train": n, "queries_per_rank": nq, "k_sweep": ks,
                        "cells_nonempty": index.n_cells, "layout": index.layout,
                        "l2": "flushed between steps (512 MB write); data 800 MB > L2",
