@@ -73,6 +73,8 @@ struct T2Args {
 struct Win {
     const float *sx;
     const float *sy;
+    const int32_t *sp;      // staged point index (perm) -- tile2d_kernel only
+    const uint8_t *sl;      // staged label code          -- tile2d_kernel only
     const int32_t *loc;     // (R, W+1) local slot of each cell start
     const int32_t *delta;   // global slot = local + delta[row]
     int R, W, W1;
@@ -86,7 +88,6 @@ struct Win {
 struct Ranges {
     int s;      // this lane's range start (staged index)
     int n;      // its length
-    int row;    // its window row (for the global slot)
     int incl;   // inclusive prefix of lengths over lanes
     int total;  // warp-uniform
 };
@@ -99,14 +100,13 @@ __device__ __forceinline__ void ranges_finish(Ranges &rg) {
 // Block(l): rows lr-l..lr+l, columns lc-l..lc+l (clipped), one row per lane.
 __device__ __forceinline__ Ranges block_ranges(const Win &w, int lr, int lc, int l) {
     const int lane = lane_id();
-    Ranges rg{0, 0, 0, 0, 0};
+    Ranges rg{0, 0, 0, 0};
     const int i = lr - l + lane;
     if (lane <= 2 * l && i >= 0 && i < w.R) {
         const int a = max(lc - l, 0), b = min(lc + l, w.W - 1);
         const int32_t *rp = w.loc + i * w.W1;
         rg.s = rp[a];
         rg.n = rp[b + 1] - rg.s;
-        rg.row = i;
     }
     ranges_finish(rg);
     return rg;
@@ -116,7 +116,7 @@ __device__ __forceinline__ Ranges block_ranges(const Win &w, int lr, int lc, int
 // lc -+ l of the rows in between (4l ranges, <= 32 for l <= 8).
 __device__ __forceinline__ Ranges shell_ranges(const Win &w, int lr, int lc, int l) {
     const int lane = lane_id();
-    Ranges rg{0, 0, 0, 0, 0};
+    Ranges rg{0, 0, 0, 0};
     if (lane < 4 * l) {
         int row, a, b;
         if (lane < 2) {
@@ -131,15 +131,14 @@ __device__ __forceinline__ Ranges shell_ranges(const Win &w, int lr, int lc, int
             const int32_t *rp = w.loc + row * w.W1;
             rg.s = rp[a];
             rg.n = rp[b + 1] - rg.s;
-            rg.row = row;
         }
     }
     ranges_finish(rg);
     return rg;
 }
 
-// Candidate m = base + lane of the flattened ranges -> staged index and row.
-__device__ __forceinline__ bool ranges_at(const Ranges &rg, int m, int &p, int &row) {
+// Candidate m = base + lane of the flattened ranges -> staged index.
+__device__ __forceinline__ bool ranges_at(const Ranges &rg, int m, int &p) {
     int L = 0;
 #pragma unroll
     for (int step = 16; step >= 1; step >>= 1) {
@@ -149,7 +148,6 @@ __device__ __forceinline__ bool ranges_at(const Ranges &rg, int m, int &p, int &
     L = L > 31 ? 31 : L;
     const int exL = __shfl_sync(GHN_FULL, rg.incl - rg.n, L);
     const int sL = __shfl_sync(GHN_FULL, rg.s, L);
-    row = __shfl_sync(GHN_FULL, rg.row, L);
     p = sL + (m - exL);
     return m < rg.total;
 }
@@ -219,14 +217,14 @@ struct Cands {
     const Ranges *rg;
     double q0, q1;
     int nch;   // warp-uniform number of 32-candidate chunks
-    // candidate i*32 + lane: key and global slot (-1 = absent)
+    // candidate i*32 + lane: key and staged index (-1 = absent)
     __device__ __forceinline__ void at(int i, double &key, int32_t &g) const {
-        int p, row;
+        int p;
         key = INFINITY;
         g = -1;
-        if (ranges_at(*rg, i * 32 + lane_id(), p, row)) {
+        if (ranges_at(*rg, i * 32 + lane_id(), p)) {
             key = key2(*w, p, q0, q1);
-            g = p + w->delta[row];
+            g = p;
         }
     }
 };
@@ -243,11 +241,11 @@ __device__ __forceinline__ Cands make_cands(const Win &w, const Ranges &rg, doub
 
 // Count member lanes into the vote: shared counters when labels are small
 // codes, else the general per-lane table.
-__device__ __forceinline__ void vote_members(const T2Args &a, WarpScratch &sc, VoteW &v, bool small,
+__device__ __forceinline__ void vote_members(const Win &w, WarpScratch &sc, VoteW &v, bool small,
                                              bool member, int32_t g) {
     const unsigned mem = __ballot_sync(GHN_FULL, member);
     if (!mem) return;
-    const int32_t L = member ? a.labels_perm[g] : -1;
+    const int32_t L = member ? (int32_t)w.sl[g] : -1;
     if (small) {
         if (member) {
             const unsigned grp = __match_any_sync(mem, L);
@@ -357,13 +355,13 @@ __device__ __forceinline__ bool select_vote_c(const T2Args &a, WarpScratch &sc, 
                     side = b2 < bs2 ? -1 : (b2 > bs2 ? 1 : 0);
                 }
             }
-            vote_members(a, sc, v, small, side < 0, cgs);
+            vote_members(*c.w, sc, v, small, side < 0, cgs);
             if (outside && __any_sync(GHN_FULL, side < 0 && (cgs < og0 || cgs >= og1))) *outside = true;
             const unsigned bnd = __ballot_sync(GHN_FULL, side == 0);
             if (side == 0) {
                 const int pos = nb + __popc(bnd & lanemask_lt());
                 sc.bkey[pos] = ckey;
-                sc.bidx[pos] = a.perm[cgs];
+                sc.bidx[pos] = c.w->sp[cgs];
                 sc.bg[pos] = cgs;
             }
             nb += __popc(bnd);
@@ -385,7 +383,7 @@ __device__ __forceinline__ bool select_vote_c(const T2Args &a, WarpScratch &sc, 
         const int32_t ti = __shfl_sync(GHN_FULL, mi, t);
         rank += lt_pair(tk, ti, mk, mi) ? 1 : 0;
     }
-    vote_members(a, sc, v, small, lane < nb && rank < r, mg);
+    vote_members(*c.w, sc, v, small, lane < nb && rank < r, mg);
     if (outside && __any_sync(GHN_FULL, lane < nb && rank < r && (mg < og0 || mg >= og1))) *outside = true;
     const unsigned kl = __ballot_sync(GHN_FULL, lane < nb && rank == r - 1);
     if (!kl) return false;
@@ -418,9 +416,9 @@ __device__ __forceinline__ int32_t vote_tiebreak_c(const T2Args &a, const Cands 
             int32_t idx = 0x7fffffff, Lb = -1;
             bool member = false;
             if (cgs >= 0 && key <= kth.key) {
-                idx = a.perm[cgs];
+                idx = c.w->sp[cgs];
                 member = key < kth.key || idx <= kth.idx;
-                if (member) Lb = a.labels_perm[cgs];
+                if (member) Lb = c.w->sl[cgs];
             }
             bool tied = false;
             for (int t = 0; t < v.used; ++t) {
@@ -534,17 +532,17 @@ __device__ __forceinline__ void process_query_k1(const T2Args &a, const Win &w, 
         double mk = INFINITY;
         int32_t mg = -1, mi = 0x7fffffff;
         for (int base = 0; base < rg.total; base += 32) {
-            int p, row;
-            if (ranges_at(rg, base + lane, p, row)) {
+            int p;
+            if (ranges_at(rg, base + lane, p)) {
                 const double key = key2(w, p, q0, q1);
-                const int32_t g = p + w.delta[row];
+                const int32_t g = p;
                 if (key < mk) {
                     mk = key;
                     mg = g;
                     mi = 0x7fffffff;
                 } else if (key == mk) {
-                    if (mi == 0x7fffffff) mi = a.perm[mg];
-                    const int32_t ii = a.perm[g];
+                    if (mi == 0x7fffffff) mi = w.sp[mg];
+                    const int32_t ii = w.sp[g];
                     if (ii < mi) {
                         mi = ii;
                         mg = g;
@@ -552,7 +550,7 @@ __device__ __forceinline__ void process_query_k1(const T2Args &a, const Win &w, 
                 }
             }
         }
-        if (mg >= 0 && mi == 0x7fffffff) mi = a.perm[mg];
+        if (mg >= 0 && mi == 0x7fffffff) mi = w.sp[mg];
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) {
             const double ok = __shfl_xor_sync(GHN_FULL, mk, off);
@@ -586,7 +584,7 @@ __device__ __forceinline__ void process_query_k1(const T2Args &a, const Win &w, 
     }
     const int64_t cells = want_stats ? block_cells(w, lr, lc, layers) : 0;
     if (lane == 0) {
-        if (a.out_label) a.out_label[qi] = a.labels_perm[cg];
+        if (a.out_label) a.out_label[qi] = (int32_t)w.sl[cg];
         if (a.out_conf) a.out_conf[qi] = 1.0;
         if (want_stats) {
             if (a.out_stats) {
@@ -654,7 +652,7 @@ __device__ __forceinline__ void process_query_w(const T2Args &a, const Win &w, W
         // fire at l = 0, so T_0 is never needed: select T_1 over block(1)
         // directly.  changed(1) <=> a member of T_1 lies outside the centre cell.
         const int32_t *rp = w.loc + lr * w.W1;
-        const int32_t og0 = rp[lc] + w.delta[lr], og1 = rp[lc + 1] + w.delta[lr];
+        const int32_t og0 = rp[lc], og1 = rp[lc + 1];   // staged range of the centre cell
         l = 1;
         blk = block_ranges(w, lr, lc, 1);
         const double e0 = fmax(q0 - (double)(a.lo0 + cc0 - 1) * a.w0, (double)(a.lo0 + cc0 + 2) * a.w0 - q0);
@@ -702,12 +700,12 @@ __device__ __forceinline__ void process_query_w(const T2Args &a, const Win &w, W
         } else {
             const Ranges sh = shell_ranges(w, lr, lc, l);
             for (int base = 0; base < sh.total; base += 32) {
-                int p, row;
-                const bool act = ranges_at(sh, base + lane, p, row);
+                int p;
+                const bool act = ranges_at(sh, base + lane, p);
                 bool lt = false;
                 if (act) {
                     const double key = key2(w, p, q0, q1);
-                    lt = key < kth.key || (key == kth.key && a.perm[p + w.delta[row]] < kth.idx);
+                    lt = key < kth.key || (key == kth.key && w.sp[p] < kth.idx);
                 }
                 below += __popc(__ballot_sync(GHN_FULL, lt));
             }
@@ -769,7 +767,9 @@ __global__ void __launch_bounds__(T2_THREADS, T2_MINB) tile2d_kernel(const T2Arg
     const int R = r_hi - r_lo + 1, W = c_hi - c_lo + 1, W1 = W + 1;
     float *sx = (float *)sm;
     float *sy = sx + a.cap;
-    int32_t *loc = (int32_t *)(sy + a.cap);                        // [R][W+1]
+    int32_t *sp = (int32_t *)(sy + a.cap);
+    uint8_t *sl = (uint8_t *)(sp + a.cap);
+    int32_t *loc = (int32_t *)(sl + a.cap);                        // [R][W+1]
     int32_t *delta = loc + a.win * (a.win + 1);                    // [R]
     int32_t *rstart = delta + a.win;                               // [R+1]
     for (int e = threadIdx.x; e < R * W1; e += blockDim.x) {
@@ -806,10 +806,12 @@ __global__ void __launch_bounds__(T2_THREADS, T2_MINB) tile2d_kernel(const T2Arg
         for (int p = p0 + (int)(threadIdx.x & 31); p < p1; p += 32) {
             sx[p] = a.c0[p + d];
             sy[p] = a.c1[p + d];
+            sp[p] = a.perm[p + d];
+            sl[p] = (uint8_t)a.labels_perm[p + d];
         }
     }
     __syncthreads();
-    Win w{sx, sy, loc, delta, R, W, W1};
+    Win w{sx, sy, sp, sl, loc, delta, R, W, W1};
     const int warp = threadIdx.x >> 5;
     const bool want_stats = a.out_stats != nullptr || a.totals != nullptr;
     for (int qq = qb + warp; qq < qe; qq += T2_THREADS / 32)
@@ -878,7 +880,7 @@ __global__ void __launch_bounds__(T2_THREADS) tile2d_grp_kernel(const T2Args a) 
         }
     }
     __syncthreads();
-    Win w{sx, sy, loc, delta, R, W, W1};
+    Win w{sx, sy, nullptr, nullptr, loc, delta, R, W, W1};
     const Grp<G> gr;
     const int gid = threadIdx.x / G;
     const bool want_stats = a.out_stats != nullptr || a.totals != nullptr;
@@ -967,7 +969,9 @@ bool tile2d_plan(const ghn_index_view *ix, int64_t nq, int32_t k, int32_t task, 
     if (cap > 8192) cap = 8192;
     if (cap < 256) cap = 256;
     plan->cap = cap;
-    plan->smem = (size_t)cap * 8 +
+    // the warp kernel also stages each point's index (int32) and label code (u8)
+    if (plan->G == 32 && !(ix->n_labels > 0 && ix->n_labels <= 256)) return false;
+    plan->smem = (size_t)cap * (plan->G == 32 ? 13 : 8) +
                  (size_t)plan->win * (plan->win + 1) * 4 + (size_t)plan->win * 4 +
                  (size_t)(plan->win + 1) * 4 + 64;
     if (plan->smem > 200 * 1024) return false;
@@ -1048,9 +1052,12 @@ int32_t tile2d_run(const ghn_index_view *ix, const Tile2dPlan *plan, const void 
     static size_t attr_smem[3] = {0, 0, 0};   // largest dynamic smem opted into, per kernel
     const int ki = plan->G == 8 ? 1 : (plan->G == 16 ? 2 : 0);
     if (plan->smem > attr_smem[ki]) {
-        if (ki == 0)
+        if (ki == 0) {
             GHN_CUDA_CHECK(cudaFuncSetAttribute(tile2d_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                 (int)plan->smem));
+            GHN_CUDA_CHECK(cudaFuncSetAttribute(tile2d_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                                (int)cudaSharedmemCarveoutMaxShared));
+        }
         else if (ki == 1)
             GHN_CUDA_CHECK(cudaFuncSetAttribute(tile2d_grp_kernel<8>,
                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)plan->smem));

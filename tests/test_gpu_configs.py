@@ -121,3 +121,17 @@ def test_tiled_group_sizes_exact(ghn, G, k, monkeypatch):
     ref = oracle.COracle(w.X, np.full(2, 1.0 / 512))
     _check_predict(ghn, index, ref, w.X, w.y, w.Q, k, "heuristic")
     _check_predict(ghn, index, ref, w.X, w.y, w.Q[:20000], k, "guaranteed")
+
+
+@pytest.mark.parametrize("n_labels", [2, 40, 200, 300])
+@pytest.mark.parametrize("k", [1, 16, 64])
+def test_label_cardinalities(ghn, n_labels, k):
+    """Vote paths by label count: shared counters (<= 32 codes), the per-warp
+    label table over staged u8 codes (<= 256), the generic kernel (> 256)."""
+    rng = np.random.default_rng(700 + n_labels)
+    X = rng.random((400_000, 2), dtype=np.float32)
+    y = rng.integers(0, n_labels, X.shape[0]).astype(np.int32)
+    Q = rng.random((30_000, 2), dtype=np.float32)
+    index = ghn.build_arrays(X, y, cells_per_axis=256)
+    ref = oracle.COracle(X, np.full(2, 1.0 / 256))
+    _check_predict(ghn, index, ref, X, y, Q, k, "heuristic")
