@@ -31,6 +31,9 @@ extern "C" {
 enum { GHN_F32 = 0, GHN_F64 = 1 };
 enum { GHN_LAYOUT_DENSE = 0, GHN_LAYOUT_LIST = 1 };
 enum { GHN_MODE_HEURISTIC = 0, GHN_MODE_GUARANTEED = 1 };           /* explore.py:21 */
+/* exact full scan (baselines.brute_knn, baselines.py:40-55; the recall
+   oracle of bench.run_bench, bench.py:160-161): every point, no grid walk */
+enum { GHN_MODE_BRUTE = 2 };
 enum { GHN_TASK_NONE = 0, GHN_TASK_CLASSIFY = 1, GHN_TASK_REGRESS_MEAN = 2, GHN_TASK_REGRESS_MEDIAN = 3 };
 enum { GHN_METRIC_EUCLIDEAN = 0, GHN_METRIC_MANHATTAN = 1, GHN_METRIC_CHEBYSHEV = 2 };   /* core.py:16 */
 enum { GHN_OK = 0, GHN_ERR_VALUE = 1, GHN_ERR_CUDA = 2, GHN_ERR_UNSUPPORTED = 3 };

@@ -16,7 +16,7 @@ LIB_PATH = os.path.join(_HERE, "libghn.so")
 GHN_MAX_DIM = 16
 GHN_F32, GHN_F64 = 0, 1
 GHN_LAYOUT_DENSE, GHN_LAYOUT_LIST = 0, 1
-GHN_MODE = {"heuristic": 0, "guaranteed": 1}
+GHN_MODE = {"heuristic": 0, "guaranteed": 1, "brute": 2}
 GHN_TASK_NONE, GHN_TASK_CLASSIFY, GHN_TASK_REGRESS_MEAN, GHN_TASK_REGRESS_MEDIAN = 0, 1, 2, 3
 GHN_METRIC = {"euclidean": 0, "manhattan": 1, "chebyshev": 2}
 GHN_OK, GHN_ERR_VALUE, GHN_ERR_CUDA, GHN_ERR_UNSUPPORTED = 0, 1, 2, 3

@@ -368,7 +368,15 @@ __device__ __forceinline__ void query_one(const QArgs &a, int64_t w) {
     tk.init();
     int64_t cells = 0, points = 0, layers = 0;
     int64_t l = lmin;
-    for (;;) {
+    if (a.mode == GHN_MODE_BRUTE) {
+        // exact full scan (baselines.py:40-55): every slot, one flattened range
+        LayerAcc acc{false, 0, 0};
+        consume<T, D, KS>(a, qd, d, 0, lane == 0 ? (int32_t)ix.n : 0, 0, 0, tk, acc);
+        cells = ix.n_cells;
+        points = ix.n;
+        l = lmax;
+    }
+    for (; a.mode != GHN_MODE_BRUTE;) {
         LayerAcc acc{false, 0, 0};
         const int64_t next = visit_layer<T, D, KS>(a, qd, r, d, l, tk, acc);
         cells += acc.cells;
@@ -656,7 +664,7 @@ extern "C" size_t ghn_query_workspace_size(const ghn_index_view *ix, int64_t nq,
 }
 
 static int32_t validate_query(const ghn_index_view *ix, int32_t k, int32_t mode) {
-    if (mode != GHN_MODE_HEURISTIC && mode != GHN_MODE_GUARANTEED) {
+    if (mode != GHN_MODE_HEURISTIC && mode != GHN_MODE_GUARANTEED && mode != GHN_MODE_BRUTE) {
         set_error("unknown mode %d", mode);
         return GHN_ERR_VALUE;
     }
@@ -758,7 +766,7 @@ extern "C" int32_t ghn_query(const ghn_index_view *ix, const void *Q, int32_t q_
     const int ks = k <= 32 ? 1 : (k <= 64 ? 2 : (k <= 128 ? 4 : 8));
     Tile2dPlan tp;
     const bool want_nb = out->dist != nullptr || out->idx != nullptr;
-    if (workspace && tile2d_plan(ix, nq, k, task, want_nb, &tp) &&
+    if (mode != GHN_MODE_BRUTE && workspace && tile2d_plan(ix, nq, k, task, want_nb, &tp) &&
         workspace_bytes >= tile2d_workspace_bytes(&tp, nq)) {
         int32_t *fb_list = nullptr, *fb_count = nullptr;
         rc = tile2d_run(ix, &tp, Q, q_dtype, nq, k, mode, out, a.inv_w, a.pow2, workspace, &fb_list,
@@ -769,7 +777,8 @@ extern "C" int32_t ghn_query(const ghn_index_view *ix, const void *Q, int32_t q_
         if (ix->dtype == GHN_F32) return launch_query<float>(a, ks, s);
         return launch_query<double>(a, ks, s);
     }
-    if (!qorder && ix->layout == GHN_LAYOUT_DENSE && nq >= BIN_MIN_QUERIES && workspace) {
+    if (mode != GHN_MODE_BRUTE && !qorder && ix->layout == GHN_LAYOUT_DENSE && nq >= BIN_MIN_QUERIES &&
+        workspace) {
         if (workspace_bytes < order_workspace_bytes(nq)) {
             set_error("query workspace too small");
             return GHN_ERR_VALUE;

@@ -62,10 +62,14 @@ def layer_cells(center, l: int) -> set[CellId]:
 
 
 def _validate(index: GridIndex, Q, k: int, mode: str):
-    import torch
-
     if mode not in STOP_MODES:
         raise ValueError(f"unknown mode {mode!r}; expected one of {STOP_MODES}")
+    return _validate_queries(index, Q, k)
+
+
+def _validate_queries(index: GridIndex, Q, k: int):
+    import torch
+
     Qt = torch.as_tensor(Q)
     if Qt.dtype not in (torch.float32, torch.float64):
         Qt = Qt.to(torch.float64)

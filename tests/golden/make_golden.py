@@ -111,11 +111,77 @@ def mean_fixture():
     np.savez_compressed(os.path.join(HERE, "mean.npz"), **out)
 
 
+def bench_fixture(ref):
+    """run_bench reports (timing stripped) produced by the reference itself on
+    seeded CSV / point inputs, plus its split and scaler outputs."""
+    import csv
+    import json
+
+    rng = np.random.default_rng(820)
+    centers = rng.uniform(-5, 5, (5, 3))
+    comp = rng.integers(0, 5, 700)
+    X = centers[comp] + rng.normal(0, 1.2, (700, 3))
+    names = ["north", "east", "south", "west", "zenith"]
+    with open(os.path.join(HERE, "bench_cls.csv"), "w", newline="") as fh:
+        wr = csv.writer(fh)
+        wr.writerow(["f0", "f1", "label", "f2"])
+        for x, c in zip(X, comp):
+            wr.writerow([repr(float(x[0])), repr(float(x[1])), names[c], repr(float(x[2]))])
+    Xr = rng.uniform(0, 10, (400, 2))
+    yr = np.sin(Xr[:, 0]) + 0.1 * Xr[:, 1] ** 2 + rng.normal(0, 0.05, 400)
+    with open(os.path.join(HERE, "bench_reg.csv"), "w", newline="") as fh:
+        wr = csv.writer(fh)
+        for x, t in zip(Xr, yr):
+            wr.writerow([repr(float(t)), repr(float(x[0])), repr(float(x[1]))])
+    Xp = np.concatenate([rng.normal(0, 1, (150, 2)), rng.normal(4, 0.7, (150, 2))])
+    yp = np.concatenate([np.zeros(150, np.int64), np.ones(150, np.int64)])
+    np.savez_compressed(os.path.join(HERE, "bench_points.npz"), X=Xp, y=yp)
+
+    cls = dict(path="bench_cls.csv", label_column="label", task="classification", has_header=True)
+    reg = dict(path="bench_reg.csv", label_column=0, task="regression", has_header=False)
+    runs = [
+        dict(spec=cls, algos=["ghn", "brute", "kdtree"], k=3, mode="heuristic", scaler_kind="standard", seed=0),
+        dict(spec=cls, algos=["ghn", "brute"], k=5, mode="guaranteed", scaler_kind="minmax", seed=3),
+        dict(spec=cls, algos=["ghn", "kdtree"], k=4, mode="heuristic", scaler_kind="none", seed=7,
+             metric="manhattan"),
+        dict(spec=reg, algos=["ghn", "brute", "kdtree"], k=4, mode="heuristic", scaler_kind="standard",
+             seed=2),
+        dict(points="bench_points.npz", task="classification", algos=["ghn", "brute"], k=3,
+             mode="heuristic", scaler_kind="standard", seed=1, split_fraction=0.7),
+    ]
+    out = []
+    for r in runs:
+        kw = {k: v for k, v in r.items() if k not in ("spec", "points")}
+        kw["algos"] = tuple(kw["algos"])
+        if "spec" in r:
+            sp = dict(r["spec"], path=os.path.join(HERE, r["spec"]["path"]))
+            data = ref.DatasetSpec(**sp)
+        else:
+            z = np.load(os.path.join(HERE, r["points"]))
+            data = ref.points_from_arrays(z["X"], z["y"].tolist())
+        rep = ref.run_bench(data, **kw)
+        from gridneighbors_ref.bench import strip_timing
+        out.append({"call": r, "report": strip_timing(rep.to_dict())})
+    with open(os.path.join(HERE, "bench_reports.json"), "w") as fh:
+        json.dump(out, fh, indent=1, sort_keys=True)
+    # split / scaler outputs on the classification CSV
+    pts = ref.load_csv(ref.DatasetSpec(os.path.join(HERE, "bench_cls.csv"), "label", "classification"))
+    tr, te = ref.split(pts, 0.8, 11)
+    sc = {kind: ref.fit_scaler(tr, kind) for kind in ("standard", "minmax", "none")}
+    np.savez_compressed(
+        os.path.join(HERE, "bench_split.npz"),
+        train_X=np.stack([p.coords for p in tr]), train_y=np.array([p.label for p in tr]),
+        test_X=np.stack([p.coords for p in te]), test_y=np.array([p.label for p in te]),
+        **{f"{k}_shift": v.shift for k, v in sc.items()}, **{f"{k}_scale": v.scale for k, v in sc.items()},
+        scaled_test=np.stack([p.coords for p in ref.apply_scaler(sc["standard"], te)]))
+
+
 def main():
     sys.path.insert(0, REPO)
     from paper_2004_02290_b200 import datagen
 
     ref = load_reference()
+    bench_fixture(ref)
     einsum_fixture()
     mean_fixture()
 
