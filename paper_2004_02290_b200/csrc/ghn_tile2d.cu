@@ -38,6 +38,9 @@ constexpr int T2_NB = 32;        // histogram buckets per select round
 constexpr int T2_SMALL = 4;      // boundary candidates ordered exactly
 constexpr int T2_NL = 4;         // distinct labels tracked by the vote
 constexpr int T2_CAP = 4096;     // staged points per tile
+#ifndef T2_EXT_MAXK
+#define T2_EXT_MAXK 16     // k at or below which phase-1 selects extract
+#endif
 #ifndef T2_MINB
 #define T2_MINB 4
 #endif
@@ -399,6 +402,105 @@ __device__ __forceinline__ bool select_vote_c(const T2Args &a, WarpScratch &sc, 
     return !v.overflow;
 }
 
+// Exact r-th smallest (key, index) by repeated warp-minimum extraction over
+// at most 32*NC candidates held in registers (block(1) at k <= 16: about 54).
+// Each round takes the warp minimum (redux.sync) of the candidates' fp32
+// round-down keys: the round-down is monotone, so a unique minimum is the
+// exact next candidate; only when round-downs collide (several lanes or
+// slots at the minimum) are the colliding candidates ranked by exact fp64
+// (key, index).  The extracted r members then vote.  Cost ~ r rounds of a
+// dozen instructions instead of the histogram passes of select_vote_c.
+template <int NC>
+__device__ __forceinline__ bool select_extract(const Win &w, WarpScratch &sc, const Ranges &rg, double q0,
+                                               double q1, int r, int lbits, Kth &out, VoteW &v,
+                                               int32_t og0, int32_t og1, bool *outside) {
+    static_assert(NC == 2, "slots kept sorted pairwise");
+    const int lane = lane_id();
+    unsigned k32[NC];
+    int pp[NC];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+        int p = 0;
+        k32[c] = 0xffffffffu;
+        if (ranges_at(rg, c * 32 + lane, p)) k32[c] = __float_as_uint(__double2float_rd(key2(w, p, q0, q1)));
+        pp[c] = p;
+    }
+    // each lane's two slots in exact (key, index) order: slot 0 is its best
+    bool swap = k32[1] < k32[0];
+    if (k32[1] == k32[0] && k32[0] != 0xffffffffu)
+        swap = lt_pair(key2(w, pp[1], q0, q1), w.sp[pp[1]], key2(w, pp[0], q0, q1), w.sp[pp[0]]);
+    if (swap) {
+        const unsigned tk = k32[0];
+        k32[0] = k32[1];
+        k32[1] = tk;
+        const int tp = pp[0];
+        pp[0] = pp[1];
+        pp[1] = tp;
+    }
+    unsigned lm = k32[0];   // this lane's next candidate (round-down key)
+    int ne = 0;             // extracted from this lane
+    int wl = 0;
+    for (int it = 0; it < r; ++it) {
+        const unsigned m = __reduce_min_sync(GHN_FULL, lm);
+        const unsigned win = __ballot_sync(GHN_FULL, lm == m);
+        if ((win & (win - 1)) == 0) {
+            wl = __ffs(win) - 1;
+        } else {
+            // colliding round-downs in several lanes: exact minimum among them
+            double rk = INFINITY;
+            int32_t ri = 0x7fffffff, rl = lane;
+            if (lm == m) {
+                const int p = ne == 0 ? pp[0] : pp[1];
+                rk = key2(w, p, q0, q1);
+                ri = w.sp[p];
+            }
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) {
+                const double ok = __shfl_xor_sync(GHN_FULL, rk, off);
+                const int32_t oi = __shfl_xor_sync(GHN_FULL, ri, off);
+                const int32_t ol = __shfl_xor_sync(GHN_FULL, rl, off);
+                if (lt_pair(ok, oi, rk, ri)) {
+                    rk = ok;
+                    ri = oi;
+                    rl = ol;
+                }
+            }
+            wl = rl;
+        }
+        if (lane == wl) {
+            ++ne;
+            lm = ne == 1 ? k32[1] : 0xffffffffu;
+        }
+    }
+    const int lastp = ne == 2 ? pp[1] : pp[0];   // meaningful on lane wl
+    unsigned memb = ne == 0 ? 0u : (ne == 1 ? 1u : 3u);
+    // the r-th member, exactly
+    const double kk = key2(w, lastp, q0, q1);
+    out.key = __shfl_sync(GHN_FULL, kk, wl);
+    out.idx = __shfl_sync(GHN_FULL, w.sp[lastp], wl);
+    v.lab = 0;
+    v.cnt = 0;
+    v.used = 0;
+    v.overflow = false;
+    sc.lcnt[lane] = 0;
+    __syncwarp();
+    bool outl = false;
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+        const bool mem = (memb >> c) & 1u;
+        vote_members(w, sc, v, lbits >= 0, mem, pp[c]);
+        outl |= mem && (pp[c] < og0 || pp[c] >= og1);
+    }
+    if (outside && __any_sync(GHN_FULL, outl)) *outside = true;
+    __syncwarp();
+    if (lbits >= 0) {
+        v.lab = lane;
+        v.cnt = sc.lcnt[lane];
+        v.used = 32;
+    }
+    return !v.overflow;
+}
+
 // Tie-break among the labels tied at the top count: the label of the member
 // minimising (sqrt(key), index) (predict.py:30-35), over the cached members.
 __device__ __forceinline__ int32_t vote_tiebreak_c(const T2Args &a, const Cands &c, const Kth &kth,
@@ -602,6 +704,7 @@ __device__ __forceinline__ void process_query_k1(const T2Args &a, const Win &w, 
     }
 }
 
+template <bool EXT>
 __device__ __forceinline__ void process_query_w(const T2Args &a, const Win &w, WarpScratch &sc, int qq,
                                                 int t0, int t1, int r_lo, int c_lo, bool want_stats) {
     const int lane = lane_id();
@@ -660,7 +763,10 @@ __device__ __forceinline__ void process_query_w(const T2Args &a, const Win &w, W
         const double hi = (e0 * e0 + e1 * e1) * (1.0 + 1e-6) + 1e-300;
         const Cands cd = make_cands(w, blk, q0, q1);
         bool outside = false;
-        if (!select_vote_c(a, sc, cd, k, 0.0, hi, kth, v, og0, og1, &outside)) {
+        const bool ok = EXT && blk.total <= 64
+                            ? select_extract<2>(w, sc, blk, q0, q1, k, a.small_labels - 1, kth, v, og0, og1, &outside)
+                            : select_vote_c(a, sc, cd, k, 0.0, hi, kth, v, og0, og1, &outside);
+        if (!ok) {
             if (lane == 0) push_fallback(a, qi);
             return;
         }
@@ -674,7 +780,10 @@ __device__ __forceinline__ void process_query_w(const T2Args &a, const Win &w, W
         const double e1 = fmax(q1 - (double)(a.lo1 + cc1 - l) * a.w1, (double)(a.lo1 + cc1 + l + 1) * a.w1 - q1);
         const double hi = (e0 * e0 + e1 * e1) * (1.0 + 1e-6) + 1e-300;
         const Cands cd = make_cands(w, blk, q0, q1);
-        if (blk.total < k || !select_vote_c(a, sc, cd, k, 0.0, hi, kth, v)) {
+        if (blk.total < k ||
+            !(EXT && blk.total <= 64 ? select_extract<2>(w, sc, blk, q0, q1, k, a.small_labels - 1, kth, v, 0,
+                                                  0x7fffffff, nullptr)
+                              : select_vote_c(a, sc, cd, k, 0.0, hi, kth, v))) {
             if (lane == 0) push_fallback(a, qi);
             return;
         }
@@ -754,6 +863,8 @@ __device__ __forceinline__ void process_query_w(const T2Args &a, const Win &w, W
     }
 }
 
+// EXT: phase-1 selects over <= 64 candidates by extraction (small k)
+template <bool EXT>
 __global__ void __launch_bounds__(T2_THREADS, T2_MINB) tile2d_kernel(const T2Args a) {
     extern __shared__ __align__(16) unsigned char sm[];
     __shared__ int s_P;
@@ -815,7 +926,7 @@ __global__ void __launch_bounds__(T2_THREADS, T2_MINB) tile2d_kernel(const T2Arg
     const int warp = threadIdx.x >> 5;
     const bool want_stats = a.out_stats != nullptr || a.totals != nullptr;
     for (int qq = qb + warp; qq < qe; qq += T2_THREADS / 32)
-        process_query_w(a, w, s_scratch[warp], qq, t0, t1, r_lo, c_lo, want_stats);
+        process_query_w<EXT>(a, w, s_scratch[warp], qq, t0, t1, r_lo, c_lo, want_stats);
 }
 
 }  // namespace
@@ -1049,29 +1160,28 @@ int32_t tile2d_run(const ghn_index_view *ix, const Tile2dPlan *plan, const void 
     a.fb_count = fbc;
     a.dbg = getenv("GHN_DEBUG_MODE") ? atoi(getenv("GHN_DEBUG_MODE")) : 0;
     a.small_labels = ix->n_labels > 0 && ix->n_labels <= 32;
-    static size_t attr_smem[3] = {0, 0, 0};   // largest dynamic smem opted into, per kernel
-    const int ki = plan->G == 8 ? 1 : (plan->G == 16 ? 2 : 0);
+    // warp kernel: extraction select for small k (EXT), histogram select otherwise
+    const int ki = plan->G == 8 ? 1 : (plan->G == 16 ? 2 : (k <= T2_EXT_MAXK ? 3 : 0));
+    static size_t attr_smem[4] = {0, 0, 0, 0};   // largest dynamic smem opted into, per kernel
     if (plan->smem > attr_smem[ki]) {
-        if (ki == 0) {
-            GHN_CUDA_CHECK(cudaFuncSetAttribute(tile2d_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                (int)plan->smem));
-            GHN_CUDA_CHECK(cudaFuncSetAttribute(tile2d_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                                (int)cudaSharedmemCarveoutMaxShared));
-        }
-        else if (ki == 1)
-            GHN_CUDA_CHECK(cudaFuncSetAttribute(tile2d_grp_kernel<8>,
-                                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)plan->smem));
-        else
-            GHN_CUDA_CHECK(cudaFuncSetAttribute(tile2d_grp_kernel<16>,
-                                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)plan->smem));
+        const void *fn = ki == 0   ? (const void *)tile2d_kernel<false>
+                         : ki == 3 ? (const void *)tile2d_kernel<true>
+                         : ki == 1 ? (const void *)tile2d_grp_kernel<8>
+                                   : (const void *)tile2d_grp_kernel<16>;
+        GHN_CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)plan->smem));
+        GHN_CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                            (int)cudaSharedmemCarveoutMaxShared));
         attr_smem[ki] = plan->smem;
     }
+    const unsigned nb = (unsigned)plan->ntiles;
     if (ki == 1)
-        tile2d_grp_kernel<8><<<(unsigned)plan->ntiles, T2_THREADS, plan->smem, s>>>(a);
+        tile2d_grp_kernel<8><<<nb, T2_THREADS, plan->smem, s>>>(a);
     else if (ki == 2)
-        tile2d_grp_kernel<16><<<(unsigned)plan->ntiles, T2_THREADS, plan->smem, s>>>(a);
+        tile2d_grp_kernel<16><<<nb, T2_THREADS, plan->smem, s>>>(a);
+    else if (ki == 3)
+        tile2d_kernel<true><<<nb, T2_THREADS, plan->smem, s>>>(a);
     else
-        tile2d_kernel<<<(unsigned)plan->ntiles, T2_THREADS, plan->smem, s>>>(a);
+        tile2d_kernel<false><<<nb, T2_THREADS, plan->smem, s>>>(a);
     GHN_LAUNCH_CHECK("tile2d_kernel");
     *fb_list = fbl;
     *fb_count = fbc;

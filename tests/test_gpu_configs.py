@@ -135,3 +135,18 @@ def test_label_cardinalities(ghn, n_labels, k):
     index = ghn.build_arrays(X, y, cells_per_axis=256)
     ref = oracle.COracle(X, np.full(2, 1.0 / 256))
     _check_predict(ghn, index, ref, X, y, Q, k, "heuristic")
+
+
+@pytest.mark.parametrize("k", [2, 4, 9, 16])
+def test_lattice_ties_exact(ghn, k):
+    """Points on a coarse lattice: many exactly equal keys (and equal fp32
+    round-downs) inside one selection -- ties resolved by point index, in
+    both the extraction and the histogram selects."""
+    rng = np.random.default_rng(808 + k)
+    X = (rng.integers(0, 300, (300_000, 2)) / 300.0).astype(np.float32)
+    Q = np.concatenate([(rng.integers(0, 300, (20_000, 2)) / 300.0 + 1 / 600.0),
+                        rng.random((20_000, 2))]).astype(np.float32)
+    y = rng.integers(0, 3, X.shape[0]).astype(np.int32)
+    index = ghn.build_arrays(X, y, cells_per_axis=256)
+    ref = oracle.COracle(X, np.full(2, 1.0 / 256))
+    _check_predict(ghn, index, ref, X, y, Q, k, "heuristic")
