@@ -439,17 +439,16 @@ __device__ __forceinline__ bool select_extract(const Win &w, WarpScratch &sc, co
     }
     unsigned lm = k32[0];   // this lane's next candidate (round-down key)
     int ne = 0;             // extracted from this lane
-    int wl = 0;
+    int lastit = -1;        // round of this lane's latest extraction
     for (int it = 0; it < r; ++it) {
         const unsigned m = __reduce_min_sync(GHN_FULL, lm);
-        const unsigned win = __ballot_sync(GHN_FULL, lm == m);
-        if ((win & (win - 1)) == 0) {
-            wl = __ffs(win) - 1;
-        } else {
+        bool mine = lm == m;
+        const unsigned win = __ballot_sync(GHN_FULL, mine);
+        if (win & (win - 1)) {
             // colliding round-downs in several lanes: exact minimum among them
             double rk = INFINITY;
             int32_t ri = 0x7fffffff, rl = lane;
-            if (lm == m) {
+            if (mine) {
                 const int p = ne == 0 ? pp[0] : pp[1];
                 rk = key2(w, p, q0, q1);
                 ri = w.sp[p];
@@ -465,13 +464,15 @@ __device__ __forceinline__ bool select_extract(const Win &w, WarpScratch &sc, co
                     rl = ol;
                 }
             }
-            wl = rl;
+            mine = lane == rl;
         }
-        if (lane == wl) {
+        if (mine) {
             ++ne;
             lm = ne == 1 ? k32[1] : 0xffffffffu;
+            lastit = it;
         }
     }
+    const int wl = __ffs(__ballot_sync(GHN_FULL, lastit == r - 1)) - 1;
     const int lastp = ne == 2 ? pp[1] : pp[0];   // meaningful on lane wl
     unsigned memb = ne == 0 ? 0u : (ne == 1 ? 1u : 3u);
     // the r-th member, exactly
