@@ -589,6 +589,22 @@ __device__ __forceinline__ bool shell_cannot_change(const T2Args &a, double q0, 
     return d * d * (1.0 - 1e-9) > kth_key;
 }
 
+// The same bound with the per-query part hoisted: the face distance of
+// block(l) is (q's distance to its own cell's nearest face) + l * w per axis.
+struct ShellBound {
+    double f0, f1, margin;
+    __device__ __forceinline__ ShellBound(const T2Args &a, double q0, double q1, int64_t cc0, int64_t cc1) {
+        f0 = fmin(q0 - (double)(a.lo0 + cc0) * a.w0, (double)(a.lo0 + cc0 + 1) * a.w0 - q0);
+        f1 = fmin(q1 - (double)(a.lo1 + cc1) * a.w1, (double)(a.lo1 + cc1 + 1) * a.w1 - q1);
+        margin = 1e-9 * fmax(a.w0, a.w1) + 1e-12 * (fabs(q0) + fabs(q1));
+    }
+    // shell(l + 1) cannot hold a point preceding kth_key
+    __device__ __forceinline__ bool cannot_change(const T2Args &a, int l, double kth_key) const {
+        const double d = fmin(f0 + (double)l * a.w0, f1 + (double)l * a.w1) - margin;
+        return d > 0.0 && d * d * (1.0 - 1e-9) > kth_key;
+    }
+};
+
 // Points in block(l) (warp-uniform; one row per lane).
 __device__ __forceinline__ int block_total(const Win &w, int lr, int lc, int l) {
     const int lane = lane_id();
@@ -759,14 +775,16 @@ __device__ __forceinline__ void process_query_w(const T2Args &a, const Win &w, W
         const int32_t og0 = rp[lc], og1 = rp[lc + 1];   // staged range of the centre cell
         l = 1;
         blk = block_ranges(w, lr, lc, 1);
-        const double e0 = fmax(q0 - (double)(a.lo0 + cc0 - 1) * a.w0, (double)(a.lo0 + cc0 + 2) * a.w0 - q0);
-        const double e1 = fmax(q1 - (double)(a.lo1 + cc1 - 1) * a.w1, (double)(a.lo1 + cc1 + 2) * a.w1 - q1);
-        const double hi = (e0 * e0 + e1 * e1) * (1.0 + 1e-6) + 1e-300;
-        const Cands cd = make_cands(w, blk, q0, q1);
         bool outside = false;
-        const bool ok = EXT && blk.total <= 64
-                            ? select_extract<2>(w, sc, blk, q0, q1, k, a.small_labels - 1, kth, v, og0, og1, &outside)
-                            : select_vote_c(a, sc, cd, k, 0.0, hi, kth, v, og0, og1, &outside);
+        bool ok;
+        if (EXT && blk.total <= 64) {
+            ok = select_extract<2>(w, sc, blk, q0, q1, k, a.small_labels - 1, kth, v, og0, og1, &outside);
+        } else {
+            const double e0 = fmax(q0 - (double)(a.lo0 + cc0 - 1) * a.w0, (double)(a.lo0 + cc0 + 2) * a.w0 - q0);
+            const double e1 = fmax(q1 - (double)(a.lo1 + cc1 - 1) * a.w1, (double)(a.lo1 + cc1 + 2) * a.w1 - q1);
+            const double hi = (e0 * e0 + e1 * e1) * (1.0 + 1e-6) + 1e-300;
+            ok = select_vote_c(a, sc, make_cands(w, blk, q0, q1), k, 0.0, hi, kth, v, og0, og1, &outside);
+        }
         if (!ok) {
             if (lane == 0) push_fallback(a, qi);
             return;
@@ -777,14 +795,16 @@ __device__ __forceinline__ void process_query_w(const T2Args &a, const Win &w, W
             if (__dmul_rn(b, b) > kth.key) stop = true;
         }
     } else {
-        const double e0 = fmax(q0 - (double)(a.lo0 + cc0 - l) * a.w0, (double)(a.lo0 + cc0 + l + 1) * a.w0 - q0);
-        const double e1 = fmax(q1 - (double)(a.lo1 + cc1 - l) * a.w1, (double)(a.lo1 + cc1 + l + 1) * a.w1 - q1);
-        const double hi = (e0 * e0 + e1 * e1) * (1.0 + 1e-6) + 1e-300;
-        const Cands cd = make_cands(w, blk, q0, q1);
-        if (blk.total < k ||
-            !(EXT && blk.total <= 64 ? select_extract<2>(w, sc, blk, q0, q1, k, a.small_labels - 1, kth, v, 0,
-                                                  0x7fffffff, nullptr)
-                              : select_vote_c(a, sc, cd, k, 0.0, hi, kth, v))) {
+        bool ok = blk.total >= k;
+        if (ok && EXT && blk.total <= 64) {
+            ok = select_extract<2>(w, sc, blk, q0, q1, k, a.small_labels - 1, kth, v, 0, 0x7fffffff, nullptr);
+        } else if (ok) {
+            const double e0 = fmax(q0 - (double)(a.lo0 + cc0 - l) * a.w0, (double)(a.lo0 + cc0 + l + 1) * a.w0 - q0);
+            const double e1 = fmax(q1 - (double)(a.lo1 + cc1 - l) * a.w1, (double)(a.lo1 + cc1 + l + 1) * a.w1 - q1);
+            const double hi = (e0 * e0 + e1 * e1) * (1.0 + 1e-6) + 1e-300;
+            ok = select_vote_c(a, sc, make_cands(w, blk, q0, q1), k, 0.0, hi, kth, v);
+        }
+        if (!ok) {
             if (lane == 0) push_fallback(a, qi);
             return;
         }
@@ -797,6 +817,7 @@ __device__ __forceinline__ void process_query_w(const T2Args &a, const Win &w, W
     int64_t points = blk.total;
     int64_t cells = want_stats ? block_cells(w, lr, lc, l) : 0;
     int layers = l;
+    const ShellBound sb(a, q0, q1, cc0, cc1);
     // phase 2: a later layer matters only if one of its points precedes the k-th
     while (!stop && l < lmax) {
         ++l;
@@ -805,8 +826,8 @@ __device__ __forceinline__ void process_query_w(const T2Args &a, const Win &w, W
             return;
         }
         int below = 0;
-        if (shell_cannot_change(a, q0, q1, cc0, cc1, l - 1, kth.key)) {
-            points += block_total(w, lr, lc, l) - block_total(w, lr, lc, l - 1);
+        if (sb.cannot_change(a, l - 1, kth.key)) {
+            if (want_stats) points += block_total(w, lr, lc, l) - block_total(w, lr, lc, l - 1);
         } else {
             const Ranges sh = shell_ranges(w, lr, lc, l);
             for (int base = 0; base < sh.total; base += 32) {
