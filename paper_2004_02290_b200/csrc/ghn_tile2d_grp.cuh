@@ -346,21 +346,24 @@ __device__ __forceinline__ void process_query_grp(const T2Args &a, const Win &w,
         double ck = INFINITY;
         int32_t ci = 0x7fffffff, cg = -1;
         bool have = false;
+        const ShellBound sbd(a, q0, q1, cc0, cc1);
         for (int l = 0;; ++l) {
             if (l > a.A) {
                 if (gr.lane == 0) push_fallback(a, qi);
                 return;
             }
-            if (have && l > 0 && shell_cannot_change(a, q0, q1, cc0, cc1, l - 1, ck)) {
-                int n = 0;
-                const int ca = max(lc - l, 0), cb = min(lc + l, w.W - 1) + 1;
-                const int ca1 = max(lc - l + 1, 0), cb1 = min(lc + l - 1, w.W - 1) + 1;
-                for (int row = max(lr - l, 0); row <= min(lr + l, w.R - 1); ++row) {
-                    const int32_t *rp = w.loc + row * w.W1;
-                    n += rp[cb] - rp[ca];
-                    if (row > lr - l && row < lr + l) n -= rp[cb1] - rp[ca1];
+            if (have && l > 0 && sbd.cannot_change(a, l - 1, ck)) {
+                if (want_stats) {
+                    int n = 0;
+                    const int ca = max(lc - l, 0), cb = min(lc + l, w.W - 1) + 1;
+                    const int ca1 = max(lc - l + 1, 0), cb1 = min(lc + l - 1, w.W - 1) + 1;
+                    for (int row = max(lr - l, 0); row <= min(lr + l, w.R - 1); ++row) {
+                        const int32_t *rp = w.loc + row * w.W1;
+                        n += rp[cb] - rp[ca];
+                        if (row > lr - l && row < lr + l) n -= rp[cb1] - rp[ca1];
+                    }
+                    points += n;
                 }
-                points += n;
                 layers = l;
                 bool stop = a.mode == GHN_MODE_HEURISTIC;
                 if (a.mode == GHN_MODE_GUARANTEED) {
