@@ -1097,7 +1097,7 @@ bool tile2d_plan(const ghn_index_view *ix, int64_t nq, int32_t k, int32_t task, 
     // staged-point capacity: the expected window plus margin (an overflowing
     // tile sends its queries to the generic kernel)
     const double expect = (double)plan->win * plan->win * rho;
-    int cap = (int)(1.2 * expect + 128.0);
+    int cap = (int)(1.1 * expect + 64.0);   // Poisson window count: +10 % is > 5 sigma at cfg4
     cap = (cap + 127) & ~127;
     if (cap > 8192) cap = 8192;
     if (cap < 256) cap = 256;
