@@ -745,7 +745,7 @@ __device__ __forceinline__ void process_query_w(const T2Args &a, const Win &w, W
     const int lr = (int)(cc0 - r_lo), lc = (int)(cc1 - c_lo);
     const int lmax = max(max((int)cc0, a.ext0 - 1 - (int)cc0), max((int)cc1, a.ext1 - 1 - (int)cc1));
     const int k = a.k;
-    if (k == 1 && a.dbg == 0) {
+    if (!EXT && k == 1 && a.dbg == 0) {
         process_query_k1(a, w, q0, q1, qi, cc0, cc1, lr, lc, lmax, want_stats);
         return;
     }
@@ -767,97 +767,102 @@ __device__ __forceinline__ void process_query_w(const T2Args &a, const Win &w, W
     bool stop = a.dbg == 2;
     Kth kth{INFINITY, 0x7fffffff};
     VoteW v{0, 0, 0, false};
-    if (l == 0 && lmax >= 1 && a.A >= 1 && a.dbg != 2) {
-        // Layer 0 filled the buffer and always `changed`; neither stop rule can
-        // fire at l = 0, so T_0 is never needed: select T_1 over block(1)
-        // directly.  changed(1) <=> a member of T_1 lies outside the centre cell.
+    // Layer 0 filled the buffer and always `changed`; neither stop rule can
+    // fire at l = 0, so T_0 is never needed: select T_1 over block(1)
+    // directly.  changed(1) <=> a member of T_1 lies outside the centre cell.
+    const bool skip0 = l == 0 && lmax >= 1 && a.A >= 1 && a.dbg != 2;
+    int32_t og0 = 0, og1 = 0x7fffffff;   // staged range of the centre cell (skip0)
+    if (skip0) {
         const int32_t *rp = w.loc + lr * w.W1;
-        const int32_t og0 = rp[lc], og1 = rp[lc + 1];   // staged range of the centre cell
+        og0 = rp[lc];
+        og1 = rp[lc + 1];
         l = 1;
         blk = block_ranges(w, lr, lc, 1);
+    }
+    if (blk.total < k) {
+        if (lane == 0) push_fallback(a, qi);
+        return;
+    }
+    int64_t points = 0, cells = 0;
+    int layers = l;
+    const ShellBound sb(a, q0, q1, cc0, cc1);
+    double hi = -1.0;   // select bucket range: < 0 = the block's own bound
+    bool first = true;
+    // One select site (code size): T_l over block(l) first, then again for
+    // every later layer that changes the top-k.
+    for (;;) {
         bool outside = false;
         bool ok;
         if (EXT && blk.total <= 64) {
             ok = select_extract<2>(w, sc, blk, q0, q1, k, a.small_labels - 1, kth, v, og0, og1, &outside);
         } else {
-            const double e0 = fmax(q0 - (double)(a.lo0 + cc0 - 1) * a.w0, (double)(a.lo0 + cc0 + 2) * a.w0 - q0);
-            const double e1 = fmax(q1 - (double)(a.lo1 + cc1 - 1) * a.w1, (double)(a.lo1 + cc1 + 2) * a.w1 - q1);
-            const double hi = (e0 * e0 + e1 * e1) * (1.0 + 1e-6) + 1e-300;
-            ok = select_vote_c(a, sc, make_cands(w, blk, q0, q1), k, 0.0, hi, kth, v, og0, og1, &outside);
+            double h = hi;
+            if (h < 0.0) {
+                const double e0 =
+                    fmax(q0 - (double)(a.lo0 + cc0 - l) * a.w0, (double)(a.lo0 + cc0 + l + 1) * a.w0 - q0);
+                const double e1 =
+                    fmax(q1 - (double)(a.lo1 + cc1 - l) * a.w1, (double)(a.lo1 + cc1 + l + 1) * a.w1 - q1);
+                h = (e0 * e0 + e1 * e1) * (1.0 + 1e-6) + 1e-300;
+            }
+            ok = select_vote_c(a, sc, make_cands(w, blk, q0, q1), k, 0.0, h, kth, v, og0, og1, &outside);
         }
         if (!ok) {
             if (lane == 0) push_fallback(a, qi);
             return;
         }
-        if (a.mode == GHN_MODE_HEURISTIC && !outside) stop = true;
-        if (a.mode == GHN_MODE_GUARANTEED) {
-            const double b = __dmul_rn(1.0, a.min_w);
-            if (__dmul_rn(b, b) > kth.key) stop = true;
+        if (first) {
+            if (skip0 && a.mode == GHN_MODE_HEURISTIC && !outside) stop = true;
+            points = blk.total;
+            cells = want_stats ? block_cells(w, lr, lc, l) : 0;
+            first = false;
         }
-    } else {
-        bool ok = blk.total >= k;
-        if (ok && EXT && blk.total <= 64) {
-            ok = select_extract<2>(w, sc, blk, q0, q1, k, a.small_labels - 1, kth, v, 0, 0x7fffffff, nullptr);
-        } else if (ok) {
-            const double e0 = fmax(q0 - (double)(a.lo0 + cc0 - l) * a.w0, (double)(a.lo0 + cc0 + l + 1) * a.w0 - q0);
-            const double e1 = fmax(q1 - (double)(a.lo1 + cc1 - l) * a.w1, (double)(a.lo1 + cc1 + l + 1) * a.w1 - q1);
-            const double hi = (e0 * e0 + e1 * e1) * (1.0 + 1e-6) + 1e-300;
-            ok = select_vote_c(a, sc, make_cands(w, blk, q0, q1), k, 0.0, hi, kth, v);
-        }
-        if (!ok) {
-            if (lane == 0) push_fallback(a, qi);
-            return;
-        }
-        // the layer that filled the buffer `changed`; the guaranteed bound may stop
+        // the layer that filled / changed the buffer `changed`; the guaranteed bound may stop
         if (a.mode == GHN_MODE_GUARANTEED) {
             const double b = __dmul_rn((double)l, a.min_w);
             if (__dmul_rn(b, b) > kth.key) stop = true;
         }
-    }
-    int64_t points = blk.total;
-    int64_t cells = want_stats ? block_cells(w, lr, lc, l) : 0;
-    int layers = l;
-    const ShellBound sb(a, q0, q1, cc0, cc1);
-    // phase 2: a later layer matters only if one of its points precedes the k-th
-    while (!stop && l < lmax) {
-        ++l;
-        if (l > a.A) {
-            if (lane == 0) push_fallback(a, qi);
-            return;
-        }
-        int below = 0;
-        if (sb.cannot_change(a, l - 1, kth.key)) {
-            if (want_stats) points += block_total(w, lr, lc, l) - block_total(w, lr, lc, l - 1);
-        } else {
-            const Ranges sh = shell_ranges(w, lr, lc, l);
-            for (int base = 0; base < sh.total; base += 32) {
-                int p;
-                const bool act = ranges_at(sh, base + lane, p);
-                bool lt = false;
-                if (act) {
-                    const double key = key2(w, p, q0, q1);
-                    lt = key < kth.key || (key == kth.key && w.sp[p] < kth.idx);
-                }
-                below += __popc(__ballot_sync(GHN_FULL, lt));
-            }
-            points += sh.total;
-        }
-        layers = l;
-        if (want_stats) cells = block_cells(w, lr, lc, l);
-        const bool changed = below > 0;
-        if (changed) {
-            blk = block_ranges(w, lr, lc, l);
-            const Cands cd = make_cands(w, blk, q0, q1);
-            if (!select_vote_c(a, sc, cd, k, 0.0, kth.key, kth, v)) {
+        // a later layer matters only if one of its points precedes the k-th
+        bool changed = false;
+        while (!stop && l < lmax) {
+            ++l;
+            if (l > a.A) {
                 if (lane == 0) push_fallback(a, qi);
                 return;
             }
+            int below = 0;
+            if (sb.cannot_change(a, l - 1, kth.key)) {
+                if (want_stats) points += block_total(w, lr, lc, l) - block_total(w, lr, lc, l - 1);
+            } else {
+                const Ranges sh = shell_ranges(w, lr, lc, l);
+                for (int base = 0; base < sh.total; base += 32) {
+                    int p;
+                    const bool act = ranges_at(sh, base + lane, p);
+                    bool lt = false;
+                    if (act) {
+                        const double key = key2(w, p, q0, q1);
+                        lt = key < kth.key || (key == kth.key && w.sp[p] < kth.idx);
+                    }
+                    below += __popc(__ballot_sync(GHN_FULL, lt));
+                }
+                points += sh.total;
+            }
+            layers = l;
+            if (want_stats) cells = block_cells(w, lr, lc, l);
+            if (below > 0) {
+                changed = true;
+                break;
+            }
+            if (a.mode == GHN_MODE_HEURISTIC) stop = true;
+            if (a.mode == GHN_MODE_GUARANTEED) {
+                const double b = __dmul_rn((double)l, a.min_w);
+                if (__dmul_rn(b, b) > kth.key) stop = true;
+            }
         }
-        if (a.mode == GHN_MODE_HEURISTIC && !changed) stop = true;
-        if (a.mode == GHN_MODE_GUARANTEED) {
-            const double b = __dmul_rn((double)l, a.min_w);
-            if (__dmul_rn(b, b) > kth.key) stop = true;
-        }
+        if (!changed) break;
+        blk = block_ranges(w, lr, lc, l);
+        hi = kth.key;
+        og0 = 0;
+        og1 = 0x7fffffff;
     }
     // winner: top count; ties -> nearest member by (sqrt(key), index)
     const int top = warp_max(lane < v.used ? v.cnt : 0);
@@ -1183,7 +1188,7 @@ int32_t tile2d_run(const ghn_index_view *ix, const Tile2dPlan *plan, const void 
     a.dbg = getenv("GHN_DEBUG_MODE") ? atoi(getenv("GHN_DEBUG_MODE")) : 0;
     a.small_labels = ix->n_labels > 0 && ix->n_labels <= 32;
     // warp kernel: extraction select for small k (EXT), histogram select otherwise
-    const int ki = plan->G == 8 ? 1 : (plan->G == 16 ? 2 : (k <= T2_EXT_MAXK ? 3 : 0));
+    const int ki = plan->G == 8 ? 1 : (plan->G == 16 ? 2 : (k >= 2 && k <= T2_EXT_MAXK ? 3 : 0));
     static size_t attr_smem[4] = {0, 0, 0, 0};   // largest dynamic smem opted into, per kernel
     if (plan->smem > attr_smem[ki]) {
         const void *fn = ki == 0   ? (const void *)tile2d_kernel<false>
