@@ -437,19 +437,23 @@ __device__ __forceinline__ bool select_extract(const Win &w, WarpScratch &sc, co
         pp[0] = pp[1];
         pp[1] = tp;
     }
-    unsigned lm = k32[0];   // this lane's next candidate (round-down key)
-    int ne = 0;             // extracted from this lane
-    int lastit = -1;        // round of this lane's latest extraction
-    for (int it = 0; it < r; ++it) {
-        const unsigned m = __reduce_min_sync(GHN_FULL, lm);
+    // lane state: lm = next candidate, nx = the one after; a consumed slot
+    // becomes TAKEN (a NaN pattern above every real key, below absent)
+    constexpr unsigned TAKEN = 0xfffffffeu;
+    unsigned lm = k32[0];
+    unsigned nx = k32[1];
+    int lastit = 0;   // countdown value of the round this lane last won
+    for (int it = r; it > 0; --it) {
+        unsigned m;
+        asm volatile("redux.sync.min.u32 %0, %1, 0xffffffff;" : "=r"(m) : "r"(lm));
         bool mine = lm == m;
         const unsigned win = __ballot_sync(GHN_FULL, mine);
-        if (win & (win - 1)) {
+        if (__builtin_expect((win & (win - 1)) != 0, 0)) {
             // colliding round-downs in several lanes: exact minimum among them
             double rk = INFINITY;
             int32_t ri = 0x7fffffff, rl = lane;
             if (mine) {
-                const int p = ne == 0 ? pp[0] : pp[1];
+                const int p = nx == TAKEN ? pp[1] : pp[0];
                 rk = key2(w, p, q0, q1);
                 ri = w.sp[p];
             }
@@ -466,13 +470,13 @@ __device__ __forceinline__ bool select_extract(const Win &w, WarpScratch &sc, co
             }
             mine = lane == rl;
         }
-        if (mine) {
-            ++ne;
-            lm = ne == 1 ? k32[1] : 0xffffffffu;
-            lastit = it;
-        }
+        // branch-free update of the winner lane
+        lm = mine ? nx : lm;
+        nx = mine ? TAKEN : nx;
+        lastit = mine ? it : lastit;
     }
-    const int wl = __ffs(__ballot_sync(GHN_FULL, lastit == r - 1)) - 1;
+    const int ne = (nx == TAKEN ? 1 : 0) + (lm == TAKEN ? 1 : 0);   // slots taken, in order
+    const int wl = __ffs(__ballot_sync(GHN_FULL, lastit == 1)) - 1;
     const int lastp = ne == 2 ? pp[1] : pp[0];   // meaningful on lane wl
     unsigned memb = ne == 0 ? 0u : (ne == 1 ? 1u : 3u);
     // the r-th member, exactly
