@@ -1214,6 +1214,12 @@ int32_t tile2d_run(const ghn_index_view *ix, const Tile2dPlan *plan, const void 
     else
         tile2d_kernel<false><<<nb, T2_THREADS, plan->smem, s>>>(a);
     GHN_LAUNCH_CHECK("tile2d_kernel");
+    if (getenv("GHN_DEBUG_FALLBACK")) {   // diagnostics: queries sent to the generic kernel
+        int32_t nfb = 0;
+        cudaMemcpyAsync(&nfb, fbc, 4, cudaMemcpyDeviceToHost, s);
+        cudaStreamSynchronize(s);
+        fprintf(stderr, "[ghn] tile2d k=%d nq=%lld fallbacks=%d\n", k, (long long)nq, nfb);
+    }
     *fb_list = fbl;
     *fb_count = fbc;
     return GHN_OK;
