@@ -567,7 +567,7 @@ __device__ __forceinline__ void query_one(const QArgs &a, int64_t w) {
 }
 
 template <typename T, int D, int KS>
-__global__ void __launch_bounds__(Q_THREADS) query_kernel(const QArgs a) {
+__global__ void __launch_bounds__(Q_THREADS, KS <= 2 ? 5 : (KS == 4 ? 3 : 2)) query_kernel(const QArgs a) {
     const int64_t nqv = a.nq_dev ? (int64_t)*a.nq_dev : a.nq;
     for (int64_t w = (int64_t)blockIdx.x * Q_WARPS + (threadIdx.x >> 5); w < nqv;
          w += (int64_t)gridDim.x * Q_WARPS)
