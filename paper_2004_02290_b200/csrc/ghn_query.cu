@@ -253,19 +253,25 @@ __device__ __forceinline__ int64_t visit_layer(const QArgs &a, const double *qd,
         int32_t s0 = 0, n0 = 0, s1 = 0, n1 = 0;
         int cells = 0;
         if (t < R) {
-            int64_t rem = t;
-            int64_t cheb = 0, rowlin = 0, mul = 1;
-            // decode: last row dim fastest; rowlin is row-major over ext[0..d-2]
+            // decode: last row dim fastest; rowlin is row-major over ext[0..d-2].
+            // DENSE: E <= 2^30, so rows, ids and the linear cell index fit 32 bits.
+            uint32_t rem = (uint32_t)t;
+            int64_t cheb = 0;
+            uint32_t rowlin = 0, mul = 1;
             for (int j = jl - 1; j >= 0; --j) {
-                const int64_t len = (int64_t)(hi_c[j] - lo_c[j] + 1);
-                const int64_t rj = lo_c[j] + (len == 1 ? 0 : rem % len);
-                rem = len == 1 ? rem : rem / len;
-                const int64_t v = iabs64(rj - r[j]);
+                const uint32_t len = (uint32_t)(hi_c[j] - lo_c[j] + 1);
+                uint32_t q = rem, rj = (uint32_t)lo_c[j];
+                if (len != 1) {
+                    q = rem / len;
+                    rj += rem - q * len;
+                }
+                rem = q;
+                const int64_t v = iabs64((int64_t)rj - r[j]);
                 cheb = v > cheb ? v : cheb;
                 rowlin += rj * mul;
-                mul *= ix.ext[j];
+                mul *= (uint32_t)ix.ext[j];
             }
-            const int64_t rowbase = rowlin * ext_last;
+            const int64_t rowbase = (int64_t)rowlin * ext_last;
             if (cheb == l) {
                 const int64_t c0 = rowbase + lo_c[jl], c1 = rowbase + hi_c[jl] + 1;
                 s0 = ix.pt_off[c0];
