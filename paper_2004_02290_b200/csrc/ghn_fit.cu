@@ -353,6 +353,102 @@ __global__ void __launch_bounds__(FIT_THREADS) scatter_records_kernel(
     }
 }
 
+// Locality pass before the cell scatter: a partition of the points by the
+// high bits of their cell key (<= 1024 key-range buckets, 4 rows of cells at
+// cfg4; measured against 256 and 4096: fewer buckets widen the scatter's
+// write window beyond L2, more shorten the partition's write runs).  Each CTA takes a contiguous chunk of points,
+// counts its buckets in shared memory, reserves one range per bucket with a
+// single global atomic, and writes compact records (coords, label, index)
+// into those ranges.  The cell scatter that follows then walks the points
+// bucket by bucket: its cursor atomics and its record writes stay inside one
+// bucket's window (L2-resident) instead of hitting all of HBM at random.
+constexpr int PART_BUCKETS = 1024;
+constexpr int PART_THREADS = 1024;
+constexpr int PART_CHUNK = 64 * PART_THREADS;
+
+template <typename T, int RWP>
+__global__ void __launch_bounds__(PART_THREADS) partition_kernel(const T *__restrict__ X, int64_t n, DimParams p,
+                                                                 int shift, const int32_t *__restrict__ labels,
+                                                                 int32_t *__restrict__ bcur,
+                                                                 uint32_t *__restrict__ part) {
+    __shared__ int cnt[PART_BUCKETS];
+    __shared__ int base[PART_BUCKETS];
+    const int64_t i0 = (int64_t)blockIdx.x * PART_CHUNK;
+    const int64_t i1 = i0 + PART_CHUNK < n ? i0 + PART_CHUNK : n;
+    for (int b = threadIdx.x; b < PART_BUCKETS; b += blockDim.x) cnt[b] = 0;
+    __syncthreads();
+    for (int64_t i = i0 + threadIdx.x; i < i1; i += blockDim.x) atomicAdd(&cnt[point_key(X, i, p) >> shift], 1);
+    __syncthreads();
+    for (int b = threadIdx.x; b < PART_BUCKETS; b += blockDim.x) {
+        const int c = cnt[b];
+        base[b] = c ? atomicAdd(&bcur[b], c) : 0;
+        cnt[b] = 0;
+    }
+    __syncthreads();
+    const int d = p.d;
+    const int cw = d * (int)(sizeof(T) / 4);
+    for (int64_t i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
+        const uint32_t b = point_key(X, i, p) >> shift;
+        const int64_t pos = (int64_t)base[b] + atomicAdd(&cnt[b], 1);
+        uint32_t w[RWP];
+#pragma unroll
+        for (int t = 0; t < RWP; ++t) w[t] = 0u;
+        const uint32_t *xs = reinterpret_cast<const uint32_t *>(X + i * d);
+#pragma unroll
+        for (int t = 0; t < RWP - 2; ++t)
+            if (t < cw) w[t] = __ldcs(xs + t);
+        w[RWP - 2] = labels ? (uint32_t)__ldcs(labels + i) : 0u;
+        w[RWP - 1] = (uint32_t)i;
+        uint4 *dst = reinterpret_cast<uint4 *>(part + pos * RWP);
+#pragma unroll
+        for (int t = 0; t < RWP / 4; ++t) dst[t] = make_uint4(w[4 * t], w[4 * t + 1], w[4 * t + 2], w[4 * t + 3]);
+    }
+}
+
+__global__ void bucket_start_kernel(const int32_t *__restrict__ pt_off, int shift, int nbuck,
+                                    int32_t *__restrict__ bcur) {
+    for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < nbuck; b += gridDim.x * blockDim.x)
+        bcur[b] = pt_off[(int64_t)b << shift];
+}
+
+// The cell scatter over the partitioned records (bucket order).
+template <typename T, int RWP, int RW>
+__global__ void __launch_bounds__(FIT_THREADS) scatter_part_kernel(const uint32_t *__restrict__ part, int64_t n,
+                                                                   DimParams p, int32_t *__restrict__ cursor,
+                                                                   uint32_t *__restrict__ rec) {
+    const int d = p.d;
+    for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < n;
+         s += (int64_t)gridDim.x * blockDim.x) {
+        uint32_t w[RW];
+#pragma unroll
+        for (int t = 0; t < RW; ++t) w[t] = 0u;
+        const uint4 *src = reinterpret_cast<const uint4 *>(part + s * RWP);
+#pragma unroll
+        for (int t = 0; t < RWP / 4; ++t) {
+            const uint4 v = __ldcs(src + t);
+            w[4 * t] = v.x;
+            w[4 * t + 1] = v.y;
+            w[4 * t + 2] = v.z;
+            w[4 * t + 3] = v.w;
+        }
+        const uint32_t lab = w[RWP - 2], idx = w[RWP - 1];
+        w[RWP - 2] = 0u;
+        w[RWP - 1] = 0u;
+        w[RW - 2] = lab;
+        w[RW - 1] = idx;
+        const T *xc = reinterpret_cast<const T *>(w);
+        uint64_t key = 0;
+        for (int j = 0; j < d; ++j) {
+            const int64_t c = cell_id(to_double(xc[j]), p.w[j], p.inv[j], (p.pow2 >> j) & 1u);
+            key = key * (uint64_t)p.ext[j] + (uint64_t)(c - p.lo[j]);
+        }
+        const int32_t slot = atomicAdd(&cursor[key], 1);
+        uint4 *dst = reinterpret_cast<uint4 *>(rec + (int64_t)slot * RW);
+#pragma unroll
+        for (int t = 0; t < RW / 4; ++t) dst[t] = make_uint4(w[4 * t], w[4 * t + 1], w[4 * t + 2], w[4 * t + 3]);
+    }
+}
+
 template <typename T, int RW>
 __global__ void __launch_bounds__(FIT_THREADS) fixup_records_kernel(
     const uint32_t *__restrict__ rec, int64_t n, DimParams p, const int32_t *__restrict__ pt_off,
@@ -424,8 +520,25 @@ __global__ void cells_from_offsets_kernel(const int32_t *__restrict__ pt_off,
 // for 100M 16-byte records vs 3.2 GB written here).
 static int record_words(int d, int dtype) {
     const int cw = d * (dtype == GHN_F32 ? 1 : 2);
-    if (cw + 2 <= 8) return 8;
+    if (cw + 2 <= 8) return 8;   // full 32-byte sectors: partial-sector scatter writes cost a DRAM read each
     return 0;   // no fast path
+}
+
+static size_t align256(size_t b) { return (b + 255) & ~(size_t)255; }
+
+// Partition records: 16 bytes when (coords, label, index) fit, else 32.
+static int part_words(int d, int dtype) {
+    const int cw = d * (dtype == GHN_F32 ? 1 : 2);
+    return cw + 2 <= 4 ? 4 : 8;
+}
+
+// Counting-scatter workspace tail: partition records, then bucket cursors.
+static size_t fast_part_off(const ghn_fit_plan *plan) {
+    const int RW = record_words(plan->d, plan->dtype);
+    return plan->fast_rec_off + align256((size_t)plan->n * RW * 4);
+}
+static size_t fast_bcur_off(const ghn_fit_plan *plan) {
+    return fast_part_off(plan) + align256((size_t)plan->n * part_words(plan->d, plan->dtype) * 4);
 }
 
 static unsigned grid_for(int64_t n, int threads = FIT_THREADS) {
@@ -442,7 +555,6 @@ static int bits_for(uint64_t maxval) {
     return b;
 }
 
-static size_t align256(size_t b) { return (b + 255) & ~(size_t)255; }
 
 template <typename T>
 int32_t bounds_launch(const T *X, int64_t n, int d, const DimParams &p, int64_t *bounds,
@@ -498,11 +610,29 @@ int32_t fit_build_impl(const ghn_fit_plan *plan, const T *X, const ghn_fit_out *
             int32_t *cursor = (int32_t *)(ws + plan->fast_cursor_off);
             uint32_t *rec = (uint32_t *)(ws + plan->fast_rec_off);
             GHN_CUDA_CHECK(cudaMemcpyAsync(cursor, out->pt_off, (size_t)E * 4, cudaMemcpyDeviceToDevice, s));
-            if (RW == 4)
-                scatter_records_kernel<T, 4><<<g, FIT_THREADS, 0, s>>>(X, n, p, cursor, out->labels_in, rec);
-            else
-                scatter_records_kernel<T, 8><<<g, FIT_THREADS, 0, s>>>(X, n, p, cursor, out->labels_in, rec);
-            GHN_LAUNCH_CHECK("scatter_records_kernel");
+            // locality pass: partition by the top key bits, then scatter bucket by bucket
+            const int kb = plan->key_bits > 0 ? plan->key_bits : 1;
+            const int shift = kb > 10 ? kb - 10 : 0;
+            const int nbuck = (int)(((E - 1) >> shift) + 1);
+            uint32_t *part = (uint32_t *)(ws + fast_part_off(plan));
+            int32_t *bcur = (int32_t *)(ws + fast_bcur_off(plan));
+            bucket_start_kernel<<<(nbuck + 255) / 256, 256, 0, s>>>(out->pt_off, shift, nbuck, bcur);
+            GHN_LAUNCH_CHECK("bucket_start_kernel");
+            const unsigned gp = (unsigned)((n + PART_CHUNK - 1) / PART_CHUNK);
+            const int RWP = part_words(d, plan->dtype);
+            if (RWP == 4) {
+                partition_kernel<T, 4><<<gp, PART_THREADS, 0, s>>>(X, n, p, shift, out->labels_in, bcur, part);
+                GHN_LAUNCH_CHECK("partition_kernel");
+                if (RW == 4)
+                    scatter_part_kernel<T, 4, 4><<<g, FIT_THREADS, 0, s>>>(part, n, p, cursor, rec);
+                else
+                    scatter_part_kernel<T, 4, 8><<<g, FIT_THREADS, 0, s>>>(part, n, p, cursor, rec);
+            } else {
+                partition_kernel<T, 8><<<gp, PART_THREADS, 0, s>>>(X, n, p, shift, out->labels_in, bcur, part);
+                GHN_LAUNCH_CHECK("partition_kernel");
+                scatter_part_kernel<T, 8, 8><<<g, FIT_THREADS, 0, s>>>(part, n, p, cursor, rec);
+            }
+            GHN_LAUNCH_CHECK("scatter_part_kernel");
             if (RW == 4)
                 fixup_records_kernel<T, 4><<<g, FIT_THREADS, 0, s>>>(rec, n, p, out->pt_off, (T *)out->coords,
                                                                       out->perm, out->labels_perm);
@@ -665,7 +795,7 @@ extern "C" int32_t ghn_fit_plan_init(ghn_fit_plan *plan, int64_t n, int32_t d, i
         const size_t base = 5 * n4 + align256(radix_workspace_bytes(n)) + align256(scan_workspace_bytes(scan_len));
         plan->fast_cursor_off = base;
         plan->fast_rec_off = base + align256((size_t)(plan->E + 1) * 4);
-        const size_t need = plan->fast_rec_off + align256((size_t)n * RW * 4);
+        const size_t need = fast_bcur_off(plan) + align256((size_t)PART_BUCKETS * 4);
         if (need > plan->workspace_bytes) plan->workspace_bytes = need;
     }
     return GHN_OK;
