@@ -70,6 +70,19 @@ def peaks():
         return 6650.0, "fallback"
 
 
+def issue_roofline():
+    """Issue-slot roofline of the predict kernel from the committed ncu capture."""
+    p = os.path.join(REPO, "profiles", "ncu_issue_r01.json")
+    try:
+        with open(p) as fh:
+            m = json.load(fh)
+        return {k: {"issue_active_frac": v["issue_active_frac"],
+                    "warp_instructions_per_query": v["warp_instructions_per_query"]}
+                for k, v in m.items() if k.startswith("k")} | {"source": "profiles/ncu_issue_r01.json"}
+    except Exception:
+        return None
+
+
 def ncu_traffic(cfg, ks):
     """Per-launch DRAM bytes of the predict kernel from the committed ncu summary."""
     p = os.path.join(REPO, "profiles", "ncu_summary.json")
@@ -452,7 +465,8 @@ def run_ours(args):
                          "traffic": ncu_traffic(cfg, ks),
                          "kernel": "ghn_query: tile2d_kernel (+ binning, + query_kernel fallbacks); "
                                    "time = whole predict call, not the kernel alone",
-                         "algorithmic_bytes_per_step": sum(algo_bytes.values())},
+                         "algorithmic_bytes_per_step": sum(algo_bytes.values()),
+                         "issue_roofline": issue_roofline()},
             "e2e": e2e,
             "gpu_launches": launches // args.steps,
             "gpu_launches_total": launches,
