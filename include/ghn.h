@@ -136,6 +136,8 @@ typedef struct ghn_index_view {
     const int32_t *labels_perm;  /* labels in CSR slot order (ghn_gather_i32), or NULL */
     int32_t n_labels;            /* label codes lie in [0, n_labels), or 0 if unknown */
     int32_t metric;              /* GHN_METRIC_*: ordering key and stop bound (core.py:72-91) */
+    double density_hint;         /* points per cell the tiled predict sizes its tiles for
+                                    (ghn_window_density); 0 = the mean n / E */
 } ghn_index_view;
 
 typedef struct ghn_query_out {
@@ -169,6 +171,15 @@ int32_t ghn_query(const ghn_index_view *ix, const void *Q, int32_t q_dtype, int6
 
 /* dst[i] = src[idx[i]] for i < n (labels into CSR slot order). */
 int32_t ghn_gather_i32(const int32_t *src, const int32_t *idx, int64_t n, int32_t *dst, void *stream);
+
+/* Local point density for tile sizing (new; no reference counterpart): for
+ * `samples` points taken at evenly spaced CSR slots (so dense regions are
+ * sampled in proportion to their points), the number of points in the
+ * (2*radius+1)^2 window of cells around the point's cell, divided by the
+ * window's cell count, written to out_density[samples] (device, fp32).
+ * 2-D DENSE indexes only (GHN_ERR_UNSUPPORTED otherwise); asynchronous. */
+int32_t ghn_window_density(const ghn_index_view *ix, int32_t radius, int32_t samples, float *out_density,
+                           void *stream);
 
 /* Number of kernels this library has launched in this process (evidence for
  * the bench's gpu_launches; monotone, thread-safe). */

@@ -34,6 +34,7 @@ EXPORTS = (
     "ghn_query_order",
     "ghn_query",
     "ghn_gather_i32",
+    "ghn_window_density",
     "ghn_launch_count",
 )
 
@@ -71,6 +72,7 @@ class IndexView(ctypes.Structure):
         ("coords", _p), ("perm", _p), ("cell_start", _p), ("cell_ids", _p),
         ("pt_off", _p), ("ne_off", _p), ("labels", _p), ("targets", _p), ("labels_perm", _p),
         ("n_labels", _i32), ("metric", _i32),
+        ("density_hint", _f64),
     ]
 
 
@@ -119,6 +121,8 @@ def lib():
     L.ghn_launch_count.restype = ctypes.c_uint64
     L.ghn_gather_i32.argtypes = [_p, _p, _i64, _p, _p]
     L.ghn_gather_i32.restype = _i32
+    L.ghn_window_density.argtypes = [_p, _i32, _i32, _p, _p]
+    L.ghn_window_density.restype = _i32
     _lib = L
     return L
 

@@ -1072,6 +1072,29 @@ __global__ void tile_scatter_kernel(const int32_t *keys, int64_t nq, const int32
 
 size_t a256(size_t b) { return (b + 255) & ~(size_t)255; }
 
+// Window density around evenly spaced CSR slots (ghn_window_density).
+__global__ void window_density_kernel(const int32_t *__restrict__ cell_start, const int32_t *__restrict__ cell_ids,
+                                      int32_t n_cells, const int32_t *__restrict__ pt_off, int64_t n,
+                                      int32_t ext0, int32_t ext1, int32_t radius, int32_t samples,
+                                      float *__restrict__ out) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= samples) return;
+    const int32_t slot = (int32_t)(((int64_t)i * n + n / 2) / samples);
+    int lo = 0, hi = n_cells - 1;   // the non-empty cell holding the slot
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (cell_start[mid] <= slot) lo = mid;
+        else hi = mid - 1;
+    }
+    const int r = cell_ids[2 * lo], c = cell_ids[2 * lo + 1];
+    const int r0 = max(r - radius, 0), r1 = min(r + radius, ext0 - 1);
+    const int c0 = max(c - radius, 0), c1 = min(c + radius, ext1 - 1);
+    int64_t cnt = 0;
+    for (int row = r0; row <= r1; ++row)
+        cnt += pt_off[(int64_t)row * ext1 + c1 + 1] - pt_off[(int64_t)row * ext1 + c0];
+    out[i] = (float)((double)cnt / ((double)(r1 - r0 + 1) * (double)(c1 - c0 + 1)));
+}
+
 }  // namespace
 
 bool tile2d_plan(const ghn_index_view *ix, int64_t nq, int32_t k, int32_t task, bool want_neighbors,
@@ -1081,7 +1104,10 @@ bool tile2d_plan(const ghn_index_view *ix, int64_t nq, int32_t k, int32_t task, 
     if (task != GHN_TASK_CLASSIFY || want_neighbors || !ix->labels_perm) return false;
     if (ix->metric != GHN_METRIC_EUCLIDEAN) return false;
     if (nq < 4096 || k < 1 || k > 256) return false;
-    const double rho = (double)ix->n / (double)ix->E;      // points per bbox cell
+    // points per cell to size tiles for: the mean, or the caller's local
+    // density quantile (ghn_window_density) when the points are clustered
+    double rho = (double)ix->n / (double)ix->E;
+    if (ix->density_hint > rho) rho = ix->density_hint;
     int lf = 0;
     while (lf < 8 && (2.0 * lf + 1) * (2.0 * lf + 1) * rho < (double)k) ++lf;
     const int A = lf + 2 > 4 ? 4 : lf + 2;
@@ -1226,3 +1252,20 @@ int32_t tile2d_run(const ghn_index_view *ix, const Tile2dPlan *plan, const void 
 }
 
 }  // namespace ghn
+
+extern "C" int32_t ghn_window_density(const ghn_index_view *ix, int32_t radius, int32_t samples,
+                                      float *out_density, void *stream) {
+    if (ix->layout != GHN_LAYOUT_DENSE || ix->d != 2) {
+        ghn::set_error("window density needs a 2-D DENSE index");
+        return GHN_ERR_UNSUPPORTED;
+    }
+    if (samples <= 0 || radius < 0 || ix->n_cells <= 0) {
+        ghn::set_error("bad window density arguments");
+        return GHN_ERR_VALUE;
+    }
+    ghn::window_density_kernel<<<(samples + 255) / 256, 256, 0, (cudaStream_t)stream>>>(
+        ix->cell_start, ix->cell_ids, ix->n_cells, ix->pt_off, ix->n, (int32_t)ix->ext[0], (int32_t)ix->ext[1],
+        radius, samples, out_density);
+    GHN_LAUNCH_CHECK("window_density_kernel");
+    return GHN_OK;
+}

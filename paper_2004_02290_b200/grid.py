@@ -250,7 +250,29 @@ class GridIndex:
         v.labels_perm = _lib.ptr(self.labels_perm)
         v.n_labels = self._labels.n_codes
         v.metric = _lib.GHN_METRIC[self.metric]
+        v.density_hint = self.density_hint(v)
         return v
+
+    def density_hint(self, v=None) -> float:
+        """Points per cell the tiled predict sizes its tiles for (2-D DENSE):
+        the 90th percentile, over points, of the mean occupancy of the 9x9
+        cells around them (ghn_window_density; one small kernel + sync the
+        first time).  Equal to the mean for uniform data, the cluster
+        density for clustered data.  0 elsewhere."""
+        if "density" not in self._cache:
+            hint = 0.0
+            if self.dim == 2 and self.plan.layout == _lib.GHN_LAYOUT_DENSE and self.n_cells > 0:
+                import torch
+
+                if v is None:
+                    v = self.view()
+                samples = int(min(4096, self.size))
+                out = torch.empty(samples, dtype=torch.float32, device=self.X.device)
+                _lib.check(_lib.lib().ghn_window_density(ctypes.byref(v), 4, samples, _lib.ptr(out),
+                                                         _lib.stream_handle()), "ghn_window_density")
+                hint = float(torch.quantile(out.double(), 0.9))
+            self._cache["density"] = hint
+        return self._cache["density"]
 
 
 def _coords_matrix(data: Sequence[LabeledPoint]) -> np.ndarray:

@@ -65,4 +65,6 @@ def test_struct_layouts_match_header():
     assert ctypes.sizeof(_lib.FitOut) == 9 * 8
     assert ctypes.sizeof(_lib.QueryOut) == 7 * 8
     assert _lib.IndexView.coords.offset == 8 + 4 * 4 + 8 + 16 * 8 + 8 + 16 * 8 * 2
+    assert _lib.IndexView.density_hint.offset == 8 + 4 * 4 + 8 + 16 * 8 + 8 + 16 * 8 * 2 + 9 * 8 + 2 * 4
+    assert ctypes.sizeof(_lib.IndexView) == 512
     assert ctypes.sizeof(_lib.FitPlan) == 8 + 4 * 4 + 8 + 16 * 8 * 3 + 8 * 3

@@ -150,3 +150,20 @@ def test_lattice_ties_exact(ghn, k):
     index = ghn.build_arrays(X, y, cells_per_axis=256)
     ref = oracle.COracle(X, np.full(2, 1.0 / 256))
     _check_predict(ghn, index, ref, X, y, Q, k, "heuristic")
+
+
+@pytest.mark.parametrize("k", [1, 7, 16, 40])
+def test_clustered_2d_density_sized_tiles(ghn, k):
+    """Clustered 2-D data: tiles sized by the local density quantile
+    (ghn_window_density) instead of the mean; still exact."""
+    rng = np.random.default_rng(950 + k)
+    means = rng.random((6, 2))
+    comp = rng.integers(0, 6, 600_000)
+    X = np.clip(means[comp] + rng.normal(0, 0.02, (600_000, 2)), 0, 1).astype(np.float32)
+    y = (comp % 3).astype(np.int32)
+    qc = rng.integers(0, 6, 30_000)
+    Q = np.clip(means[qc] + rng.normal(0, 0.02, (30_000, 2)), 0, 1).astype(np.float32)
+    index = ghn.build_arrays(X, y, cells_per_axis=512)
+    assert index.density_hint() > 3 * X.shape[0] / (512 * 512)
+    ref = oracle.COracle(X, np.full(2, 1.0 / 512))
+    _check_predict(ghn, index, ref, X, y, Q, k, "heuristic")
