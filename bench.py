@@ -54,7 +54,7 @@ def parse_args(argv=None):
     ap.add_argument("--ks", type=str, default=None, help="k sweep, default: the config's")
     ap.add_argument("--n", type=int, default=None, help="override n_train (debug only)")
     ap.add_argument("--nq", type=int, default=None, help="override queries per rank (debug only)")
-    ap.add_argument("--cpu-sample", type=int, default=1, help="port queries per k for cpu_baseline")
+    ap.add_argument("--cpu-sample", type=int, default=4, help="port queries per k for cpu_baseline (~10 s)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     return ap.parse_args(argv)

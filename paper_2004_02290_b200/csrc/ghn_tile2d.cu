@@ -27,6 +27,8 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <mutex>
+
 #include "ghn_common.cuh"
 #include "ghn_tile2d.cuh"
 
@@ -1219,8 +1221,14 @@ int32_t tile2d_run(const ghn_index_view *ix, const Tile2dPlan *plan, const void 
     a.small_labels = ix->n_labels > 0 && ix->n_labels <= 32;
     // warp kernel: extraction select for small k (EXT), histogram select otherwise
     const int ki = plan->G == 8 ? 1 : (plan->G == 16 ? 2 : (k >= 2 && k <= T2_EXT_MAXK ? 3 : 0));
-    static size_t attr_smem[4] = {0, 0, 0, 0};   // largest dynamic smem opted into, per kernel
-    if (plan->smem > attr_smem[ki]) {
+    // largest dynamic smem opted into, per device and kernel (function
+    // attributes are per device; callers may run on several devices / threads)
+    static std::mutex attr_mu;
+    static size_t attr_smem[64][4] = {};
+    int dev = 0;
+    GHN_CUDA_CHECK(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> attr_lock(attr_mu);
+    if (dev >= 0 && dev < 64 && plan->smem > attr_smem[dev][ki]) {
         const void *fn = ki == 0   ? (const void *)tile2d_kernel<false>
                          : ki == 3 ? (const void *)tile2d_kernel<true>
                          : ki == 1 ? (const void *)tile2d_grp_kernel<8>
@@ -1228,7 +1236,7 @@ int32_t tile2d_run(const ghn_index_view *ix, const Tile2dPlan *plan, const void 
         GHN_CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)plan->smem));
         GHN_CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout,
                                             (int)cudaSharedmemCarveoutMaxShared));
-        attr_smem[ki] = plan->smem;
+        attr_smem[dev][ki] = plan->smem;
     }
     const unsigned nb = (unsigned)plan->ntiles;
     if (ki == 1)

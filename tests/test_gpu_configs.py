@@ -167,3 +167,40 @@ def test_clustered_2d_density_sized_tiles(ghn, k):
     assert index.density_hint() > 3 * X.shape[0] / (512 * 512)
     ref = oracle.COracle(X, np.full(2, 1.0 / 512))
     _check_predict(ghn, index, ref, X, y, Q, k, "heuristic")
+
+
+def test_concurrent_readers_on_streams(ghn):
+    """Any number of concurrent readers of a built index (SPEC: concurrent
+    reads): two host threads predicting on their own CUDA streams get the
+    single-threaded answers."""
+    import threading
+
+    import torch
+
+    from paper_2004_02290_b200 import datagen
+
+    w = datagen.cfg4(n=2_000_000, nq=80_000, seed=77)
+    index = ghn.build_arrays(w.X, w.y, cells_per_axis=1024)
+    Q = torch.from_numpy(w.Q).cuda()
+    want = {k: ghn.predict_batch(index, Q, k)["label"].cpu() for k in (1, 5, 16, 33)}
+    got, errs = {}, []
+
+    def run(ks):
+        try:
+            st = torch.cuda.Stream()
+            with torch.cuda.stream(st):
+                for _ in range(3):
+                    for k in ks:
+                        got[k] = ghn.predict_batch(index, Q, k, stream=st)["label"]
+            st.synchronize()
+        except Exception as e:   # pragma: no cover - reported below
+            errs.append(e)
+
+    ts = [threading.Thread(target=run, args=(ks,)) for ks in ((1, 16), (5, 33))]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errs
+    for k in want:
+        assert torch.equal(got[k].cpu(), want[k])
