@@ -40,6 +40,9 @@ constexpr int T2_NB = 32;        // histogram buckets per select round
 constexpr int T2_SMALL = 4;      // boundary candidates ordered exactly
 constexpr int T2_NL = 4;         // distinct labels tracked by the vote
 constexpr int T2_CAP = 4096;     // staged points per tile
+constexpr int TT_KMAX = 32;      // thread-per-query kernel: largest k
+constexpr double TT_Q = 384.0;   // thread-per-query kernel: queries per tile
+constexpr double TT_CAP = 8192.0;
 #ifndef T2_EXT_MAXK
 #define T2_EXT_MAXK 16     // k at or below which phase-1 selects extract
 #endif
@@ -73,6 +76,7 @@ struct T2Args {
     int32_t *fb_count;
     int32_t dbg;
     int32_t small_labels;
+    int32_t lmask;   // label-code mask of the thread kernel (2^LB - 1)
 };
 
 struct Win {
@@ -966,6 +970,7 @@ __global__ void __launch_bounds__(T2_THREADS, T2_MINB) tile2d_kernel(const T2Arg
 }  // namespace ghn
 
 #include "ghn_tile2d_grp.cuh"
+#include "ghn_tile2d_thr.cuh"
 
 namespace ghn {
 namespace {
@@ -1130,7 +1135,26 @@ bool tile2d_plan(const ghn_index_view *ix, int64_t nq, int32_t k, int32_t task, 
     // The group kernel votes with shared counters: label codes in [0, 32).
     plan->G = 32;
     if (k == 1 && ix->n_labels > 0 && ix->n_labels <= 32) plan->G = 8;
+    // thread per query (packed-key register list): k <= 32, <= 8 label codes
+    if (k <= TT_KMAX && ix->n_labels > 0 && ix->n_labels <= 8) plan->G = 1;
     if (getenv("GHN_TILE_G")) plan->G = atoi(getenv("GHN_TILE_G"));
+    if (plan->G == 1) {
+        // ~TT_Q queries per tile (one or two per thread) within the staging capacity
+        const double qd = (double)nq / (double)ix->E;
+        const double tq = getenv("GHN_TT_Q") ? atof(getenv("GHN_TT_Q")) : TT_Q;
+        int Tq = (int)floor(sqrt(tq / (qd > 1e-9 ? qd : 1e-9)));
+        const int Tc = (int)floor(sqrt((TT_CAP - 64.0) / 1.1 / (rho > 1e-9 ? rho : 1e-9))) - 2 * A;
+        if (Tq > Tc) Tq = Tc;
+        if (Tq > Tmax) Tq = (int)Tmax;
+        if (Tq > 64) Tq = 64;
+        if (Tq < 1) return false;
+        T = Tq;
+        plan->T = T;
+        plan->nt0 = (int32_t)((ix->ext[0] + T - 1) / T);
+        plan->nt1 = (int32_t)((ix->ext[1] + T - 1) / T);
+        plan->ntiles = (int64_t)plan->nt0 * plan->nt1;
+        plan->win = T + 2 * A;
+    }
     // staged-point capacity: the expected window plus margin (an overflowing
     // tile sends its queries to the generic kernel)
     const double expect = (double)plan->win * plan->win * rho;
@@ -1139,6 +1163,11 @@ bool tile2d_plan(const ghn_index_view *ix, int64_t nq, int32_t k, int32_t task, 
     if (cap > 8192) cap = 8192;
     if (cap < 256) cap = 256;
     plan->cap = cap;
+    if (plan->G == 1) {   // float2 coordinates + u8 label code per staged point
+        plan->smem = (size_t)cap * 9 + (size_t)plan->win * (plan->win + 1) * 4 + (size_t)plan->win * 4 +
+                     (size_t)(plan->win + 1) * 4 + 64;
+        return plan->smem <= 200 * 1024;
+    }
     // the warp kernel also stages each point's index (int32) and label code (u8)
     if (plan->G == 32 && !(ix->n_labels > 0 && ix->n_labels <= 256)) return false;
     plan->smem = (size_t)cap * (plan->G == 32 ? 13 : 8) +
@@ -1219,27 +1248,45 @@ int32_t tile2d_run(const ghn_index_view *ix, const Tile2dPlan *plan, const void 
     a.fb_count = fbc;
     a.dbg = getenv("GHN_DEBUG_MODE") ? atoi(getenv("GHN_DEBUG_MODE")) : 0;
     a.small_labels = ix->n_labels > 0 && ix->n_labels <= 32;
+    a.lmask = ix->n_labels <= 2 ? 1 : (ix->n_labels <= 4 ? 3 : 7);
+    const bool stats = out->stats != nullptr || out->totals != nullptr;
     // warp kernel: extraction select for small k (EXT), histogram select otherwise
-    const int ki = plan->G == 8 ? 1 : (plan->G == 16 ? 2 : (k >= 2 && k <= T2_EXT_MAXK ? 3 : 0));
+    int ki = plan->G == 8 ? 1 : (plan->G == 16 ? 2 : (k >= 2 && k <= T2_EXT_MAXK ? 3 : 0));
+    const void *fn = ki == 0   ? (const void *)tile2d_kernel<false>
+                     : ki == 3 ? (const void *)tile2d_kernel<true>
+                     : ki == 1 ? (const void *)tile2d_grp_kernel<8>
+                               : (const void *)tile2d_grp_kernel<16>;
+    if (plan->G == 1) {   // thread per query: list capacity KM = next power of two >= k
+        int lk = 0;
+        while ((1 << lk) < k) ++lk;
+        ki = 4 + 2 * lk + (stats ? 1 : 0);
+        static const void *const thr_fns[12] = {
+            (const void *)tile2d_thr_kernel<1, false>,  (const void *)tile2d_thr_kernel<1, true>,
+            (const void *)tile2d_thr_kernel<2, false>,  (const void *)tile2d_thr_kernel<2, true>,
+            (const void *)tile2d_thr_kernel<4, false>,  (const void *)tile2d_thr_kernel<4, true>,
+            (const void *)tile2d_thr_kernel<8, false>,  (const void *)tile2d_thr_kernel<8, true>,
+            (const void *)tile2d_thr_kernel<16, false>, (const void *)tile2d_thr_kernel<16, true>,
+            (const void *)tile2d_thr_kernel<32, false>, (const void *)tile2d_thr_kernel<32, true>};
+        fn = thr_fns[ki - 4];
+    }
     // largest dynamic smem opted into, per device and kernel (function
     // attributes are per device; callers may run on several devices / threads)
     static std::mutex attr_mu;
-    static size_t attr_smem[64][4] = {};
+    static size_t attr_smem[64][16] = {};
     int dev = 0;
     GHN_CUDA_CHECK(cudaGetDevice(&dev));
     std::lock_guard<std::mutex> attr_lock(attr_mu);
     if (dev >= 0 && dev < 64 && plan->smem > attr_smem[dev][ki]) {
-        const void *fn = ki == 0   ? (const void *)tile2d_kernel<false>
-                         : ki == 3 ? (const void *)tile2d_kernel<true>
-                         : ki == 1 ? (const void *)tile2d_grp_kernel<8>
-                                   : (const void *)tile2d_grp_kernel<16>;
         GHN_CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)plan->smem));
         GHN_CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout,
                                             (int)cudaSharedmemCarveoutMaxShared));
         attr_smem[dev][ki] = plan->smem;
     }
     const unsigned nb = (unsigned)plan->ntiles;
-    if (ki == 1)
+    if (ki >= 4) {
+        void *args[] = {&a};
+        GHN_CUDA_CHECK(cudaLaunchKernel(fn, dim3(nb), dim3(TT_THREADS), args, plan->smem, s));
+    } else if (ki == 1)
         tile2d_grp_kernel<8><<<nb, T2_THREADS, plan->smem, s>>>(a);
     else if (ki == 2)
         tile2d_grp_kernel<16><<<nb, T2_THREADS, plan->smem, s>>>(a);

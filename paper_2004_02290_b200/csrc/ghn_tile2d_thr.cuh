@@ -1,0 +1,343 @@
+// ghn_tile2d_thr.cuh -- thread-per-query variant of the tiled 2-D classify
+// (explore.py:66-137 + predict.py:20-36), for k <= 32 and <= 8 label codes.
+//
+// Each thread answers one query over the staged window with a register-
+// resident list of the k+1 smallest PACKED keys of the candidates seen:
+//
+//   packed = bits[62..31] of the fp64 key (exponent + 21 mantissa bits; the
+//            sign is 0), low LB bits replaced by the label code.
+//
+// Truncating the IEEE pattern of a non-negative double is monotone, so the
+// "d-part" (packed >> LB) of a key is a non-decreasing function of the exact
+// key: sorting candidates by exact (key, index) also sorts them by d-part.
+// Hence, with tau = the k-th smallest packed value and D(.) the d-part:
+//   * the k smallest d-parts are exactly the d-parts of the exact top-k, and
+//     D(tau) = D(exact k-th key);
+//   * a shell point precedes the exact k-th iff D(p) < D(tau) when
+//     D(p) != D(tau) (explore.py:117 `changed`);
+//   * when D(list[k]) > D(tau) the top-k SET is {candidates with D <= D(tau)}
+//     and the list holds exactly their labels, so the vote reads the list.
+// Every case the d-parts cannot decide (equal d-parts across the k-th
+// boundary, a guaranteed-stop bound inside the k-th key's d-part interval,
+// a vote tie-break between members less than two d-units apart) sends the
+// query to the generic exact kernel -- rare (keys must agree to ~2^-18
+// relative) and always correct.
+//
+// The list update is a branch-free min/max bubble (2 integer ops per slot),
+// so the 32 queries of a warp advance in lock-step over their candidates;
+// only their candidate counts differ.  Included by ghn_tile2d.cu after the
+// shared helpers (T2Args, ShellBound, push_fallback).
+#pragma once
+
+namespace ghn {
+namespace {
+
+constexpr int TT_THREADS = 256;
+constexpr uint32_t TT_INF = 0xffffffffu;
+
+struct ThrWin {
+    const float2 *xy;      // staged coordinates
+    const uint8_t *sl;     // staged label codes
+    const int32_t *loc;    // (R, W+1) local slot of each cell start
+    int R, W, W1;
+};
+
+// Range r of shell(l) (l = 0: the centre cell; l >= 1: 4l ranges -- the full
+// rows lr -+ l, then the side cells lc -+ l of the rows in between), clipped
+// to the window (which holds every in-grid cell within the apron).
+__device__ __forceinline__ void thr_shell_range(const ThrWin &w, int lr, int lc, int l, int r, int &s, int &e) {
+    int row, ca, cb;
+    if (l == 0) {
+        row = lr;
+        ca = cb = lc;
+    } else if (r < 2) {
+        row = r == 0 ? lr - l : lr + l;
+        ca = max(lc - l, 0);
+        cb = min(lc + l, w.W - 1);
+    } else {
+        row = lr - l + 1 + ((r - 2) >> 1);
+        ca = cb = ((r - 2) & 1) ? lc + l : lc - l;
+    }
+    s = e = 0;
+    if (row >= 0 && row < w.R && ca >= 0 && cb < w.W && ca <= cb) {
+        const int32_t *rp = w.loc + row * w.W1;
+        s = rp[ca];
+        e = rp[cb + 1];
+    }
+}
+
+__device__ __forceinline__ int thr_shell_count(const ThrWin &w, int lr, int lc, int l) {
+    const int nr = l == 0 ? 1 : 4 * l;
+    int n = 0;
+    for (int r = 0; r < nr; ++r) {
+        int s, e;
+        thr_shell_range(w, lr, lc, l, r, s, e);
+        n += e - s;
+    }
+    return n;
+}
+
+__device__ __forceinline__ int thr_block_cells(const ThrWin &w, int lr, int lc, int l) {
+    int cells = 0;
+    for (int row = max(lr - l, 0); row <= min(lr + l, w.R - 1); ++row) {
+        const int32_t *rp = w.loc + row * w.W1;
+        for (int c = max(lc - l, 0); c <= min(lc + l, w.W - 1); ++c) cells += rp[c + 1] > rp[c];
+    }
+    return cells;
+}
+
+// Packed key of a staged point: numpy einsum order for d = 2 (core.py:80;
+// SURVEY Appendix A.3): d0^2 + d1^2, separate roundings, no FMA.
+__device__ __forceinline__ uint32_t thr_pack(float2 c, double q0, double q1, uint32_t lab, uint32_t lmask) {
+    const double d0 = __dsub_rn((double)c.x, q0);
+    const double d1 = __dsub_rn((double)c.y, q1);
+    const double key = __dadd_rn(__dmul_rn(d0, d0), __dmul_rn(d1, d1));
+    const uint32_t top = __funnelshift_l((uint32_t)__double2loint(key), (uint32_t)__double2hiint(key), 1);
+    return (top & ~lmask) | lab;
+}
+
+// Keys whose d-part is D (label bits cleared) lie in [lower, upper).
+__device__ __forceinline__ double thr_lower(uint32_t dm) {
+    return __longlong_as_double((long long)((uint64_t)dm << 31));
+}
+__device__ __forceinline__ double thr_upper(uint32_t dm, uint32_t lmask) {
+    return __longlong_as_double((long long)(((uint64_t)dm + lmask + 1u) << 31));
+}
+
+template <int N>
+__device__ __forceinline__ void thr_bubble(uint32_t (&L)[N], uint32_t v) {
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+        const uint32_t m = min(L[j], v);
+        v = max(L[j], v);
+        L[j] = m;
+    }
+}
+
+template <int N>
+__device__ __forceinline__ uint32_t thr_pick(const uint32_t (&L)[N], int j) {
+    uint32_t v = L[0];
+#pragma unroll
+    for (int i = 1; i < N; ++i) v = i == j ? L[i] : v;
+    return v;
+}
+
+struct ThrTotals {
+    unsigned long long layers, cells, points, n;
+};
+
+// One query on one thread.  False = sent to the generic kernel.
+template <int KM, bool STATS>
+__device__ __forceinline__ void process_query_thr(const T2Args &a, const ThrWin &w, int32_t qi, int t0, int t1,
+                                                  int r_lo, int c_lo, ThrTotals &tot) {
+    double q0, q1;
+    if (a.q_dtype == GHN_F32) {
+        const float2 qf = ((const float2 *)a.Q)[qi];
+        q0 = (double)qf.x;
+        q1 = (double)qf.y;
+    } else {
+        q0 = ((const double *)a.Q)[2 * (int64_t)qi];
+        q1 = ((const double *)a.Q)[2 * (int64_t)qi + 1];
+    }
+    const int64_t cc0 = cell_id(q0, a.w0, a.inv0, a.pow2 & 1u) - a.lo0;
+    const int64_t cc1 = cell_id(q1, a.w1, a.inv1, (a.pow2 >> 1) & 1u) - a.lo1;
+    const int64_t tr0 = (int64_t)t0 * a.T, tc0 = (int64_t)t1 * a.T;
+    if (cc0 < tr0 || cc0 >= tr0 + a.T || cc1 < tc0 || cc1 >= tc0 + a.T || cc0 >= a.ext0 || cc1 >= a.ext1) {
+        push_fallback(a, qi);   // centre outside the grid
+        return;
+    }
+    const int lr = (int)(cc0 - r_lo), lc = (int)(cc1 - c_lo);
+    const int lmax = max(max((int)cc0, a.ext0 - 1 - (int)cc0), max((int)cc1, a.ext1 - 1 - (int)cc1));
+    const int k = a.k;
+    const uint32_t lmask = (uint32_t)a.lmask;
+    uint32_t L[KM + 1];
+#pragma unroll
+    for (int j = 0; j <= KM; ++j) L[j] = TT_INF;
+    const ShellBound sb(a, q0, q1, cc0, cc1);
+    int cnt = 0, layers = 0;
+    int64_t points = 0;
+    for (int l = 0;; ++l) {
+        if (l > a.A) {
+            push_fallback(a, qi);
+            return;
+        }
+        const bool full_prev = cnt >= k;
+        const uint32_t tm = full_prev ? (thr_pick(L, k - 1) & ~lmask) : 0u;
+        bool changed;
+        if (full_prev && sb.cannot_change(a, l - 1, thr_upper(tm, lmask))) {
+            // shell(l) cannot hold a point preceding the k-th (counted, not scanned)
+            if (STATS) points += thr_shell_count(w, lr, lc, l);
+            changed = false;
+        } else {
+            const int nr = l == 0 ? 1 : 4 * l;
+            int r = 0, p, e;
+            thr_shell_range(w, lr, lc, l, 0, p, e);
+            bool lt = false, eq = false;
+            int ns = 0;
+            for (;;) {
+                while (p >= e) {
+                    if (++r >= nr) break;
+                    thr_shell_range(w, lr, lc, l, r, p, e);
+                }
+                if (p >= e) break;
+                const uint32_t pk = thr_pack(w.xy[p], q0, q1, (uint32_t)w.sl[p], lmask);
+                lt |= pk < tm;
+                eq |= (uint32_t)(pk - tm) <= lmask;
+                thr_bubble(L, pk);
+                ++ns;
+                ++p;
+            }
+            if (full_prev && eq) {   // a shell point shares the k-th key's d-part
+                push_fallback(a, qi);
+                return;
+            }
+            cnt += ns;
+            if (STATS) points += ns;
+            changed = full_prev ? lt : ns > 0;
+        }
+        layers = l;
+        bool stop = false;
+        if (cnt >= k) {
+            if (a.mode == GHN_MODE_HEURISTIC && !changed) stop = true;
+            if (a.mode == GHN_MODE_GUARANTEED) {
+                const double b = __dmul_rn((double)l, a.min_w);
+                const double b2 = __dmul_rn(b, b);
+                const uint32_t tk = thr_pick(L, k - 1) & ~lmask;
+                if (b2 >= thr_upper(tk, lmask)) stop = true;
+                else if (b2 > thr_lower(tk)) {   // bound inside the k-th key's interval
+                    push_fallback(a, qi);
+                    return;
+                }
+            }
+        }
+        if (stop || l >= lmax) break;
+    }
+    // top-k set = the list's first k entries unless the (k+1)-th shares the k-th's d-part
+    const uint32_t tau = thr_pick(L, k - 1), nx = thr_pick(L, k);
+    if (nx != TT_INF && (nx & ~lmask) == (tau & ~lmask)) {
+        push_fallback(a, qi);
+        return;
+    }
+    // vote (predict.py:29-36): 8-bit counters per label code
+    uint64_t cn = 0;
+#pragma unroll
+    for (int j = 0; j < KM; ++j)
+        if (j < k) cn += 1ull << (8 * (L[j] & lmask));
+    int top = 0, ntie = 0, wl = 0;
+    for (int lab = 0; lab <= (int)lmask; ++lab) {
+        const int c = (int)((cn >> (8 * lab)) & 0xffu);
+        if (c > top) {
+            top = c;
+            wl = lab;
+            ntie = 1;
+        } else if (c == top && c > 0) {
+            ++ntie;
+        }
+    }
+    if (ntie > 1) {
+        // the tied label of the member minimising (sqrt(key), index): the
+        // first tied entry of the list, provided the first tied entry of
+        // another label is >= 2 d-units behind it (then its key, and its
+        // sqrt, is strictly larger)
+        uint32_t w1 = TT_INF, w2 = TT_INF;
+#pragma unroll
+        for (int j = 0; j < KM; ++j) {
+            const uint32_t lab = L[j] & lmask;
+            const bool tied = j < k && (int)((cn >> (8 * lab)) & 0xffu) == top;
+            if (tied && w1 == TT_INF) w1 = L[j];
+            else if (tied && w2 == TT_INF && lab != (w1 & lmask)) w2 = L[j];
+        }
+        const int lb = __popc(lmask);
+        if ((w2 >> lb) - (w1 >> lb) < 2u) {
+            push_fallback(a, qi);
+            return;
+        }
+        wl = (int)(w1 & lmask);
+    }
+    if (a.out_label) a.out_label[qi] = wl;
+    if (a.out_conf) a.out_conf[qi] = __ddiv_rn((double)top, (double)k);
+    if (STATS) {
+        const int cells = thr_block_cells(w, lr, lc, layers);
+        if (a.out_stats) {
+            a.out_stats[3 * (int64_t)qi + 0] = layers;
+            a.out_stats[3 * (int64_t)qi + 1] = cells;
+            a.out_stats[3 * (int64_t)qi + 2] = points;
+        }
+        tot.layers += layers;
+        tot.cells += cells;
+        tot.points += points;
+        tot.n += 1;
+    }
+}
+
+template <int KM, bool STATS>
+__global__ void __launch_bounds__(TT_THREADS) tile2d_thr_kernel(const T2Args a) {
+    extern __shared__ __align__(16) unsigned char sm[];
+    __shared__ int s_P;
+    const int t = blockIdx.x;
+    const int qb = a.tile_start[t], qe = a.tile_start[t + 1];
+    if (qb == qe) return;
+    const int t0 = t / a.nt1, t1 = t - (t / a.nt1) * a.nt1;
+    const int r_lo = max(t0 * a.T - a.A, 0), r_hi = min(t0 * a.T + a.T - 1 + a.A, a.ext0 - 1);
+    const int c_lo = max(t1 * a.T - a.A, 0), c_hi = min(t1 * a.T + a.T - 1 + a.A, a.ext1 - 1);
+    const int R = r_hi - r_lo + 1, W = c_hi - c_lo + 1, W1 = W + 1;
+    float2 *sxy = (float2 *)sm;
+    uint8_t *sl = (uint8_t *)(sxy + a.cap);
+    int32_t *loc = (int32_t *)(sl + a.cap);                        // [R][W+1]
+    int32_t *delta = loc + a.win * (a.win + 1);                    // [R]
+    int32_t *rstart = delta + a.win;                               // [R+1]
+    for (int e = threadIdx.x; e < R * W1; e += blockDim.x) {
+        const int i = e / W1, j = e - (e / W1) * W1;
+        loc[e] = a.pt_off[(int64_t)(r_lo + i) * a.ext1 + c_lo + j];
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {   // row prefix by one warp, 32 rows at a time
+        int carry = 0;
+        for (int i0 = 0; i0 < R; i0 += 32) {
+            const int i = i0 + (int)threadIdx.x;
+            const int len = i < R ? loc[i * W1 + W] - loc[i * W1] : 0;
+            const int inc = warp_inclusive_scan(len);
+            if (i < R) {
+                rstart[i] = carry + inc - len;
+                delta[i] = loc[i * W1] - (carry + inc - len);
+            }
+            carry += __shfl_sync(GHN_FULL, inc, 31);
+        }
+        if (threadIdx.x == 0) {
+            rstart[R] = carry;
+            s_P = carry;
+        }
+    }
+    __syncthreads();
+    const int P = s_P;
+    if (P > a.cap) {
+        for (int qq = qb + threadIdx.x; qq < qe; qq += blockDim.x) push_fallback(a, a.qorder[qq]);
+        return;
+    }
+    for (int e = threadIdx.x; e < R * W1; e += blockDim.x) loc[e] -= delta[e / W1];
+    for (int i = threadIdx.x >> 5; i < R; i += TT_THREADS / 32) {   // warp per row: coalesced copy
+        const int p0 = rstart[i], p1 = rstart[i + 1], d = delta[i];
+        for (int p = p0 + (int)(threadIdx.x & 31); p < p1; p += 32) {
+            sxy[p] = make_float2(__ldg(a.c0 + p + d), __ldg(a.c1 + p + d));
+            sl[p] = (uint8_t)__ldg(a.labels_perm + p + d);
+        }
+    }
+    __syncthreads();
+    const ThrWin w{sxy, sl, loc, R, W, W1};
+    ThrTotals tot{0, 0, 0, 0};
+    for (int qq = qb + (int)threadIdx.x; qq < qe; qq += TT_THREADS)
+        process_query_thr<KM, STATS>(a, w, a.qorder[qq], t0, t1, r_lo, c_lo, tot);
+    if (STATS && a.totals) {
+        const unsigned long long v0 = warp_sum(tot.layers), v1 = warp_sum(tot.cells), v2 = warp_sum(tot.points),
+                                 v3 = warp_sum(tot.n);
+        if ((threadIdx.x & 31) == 0 && v3) {
+            atomicAdd(&a.totals[0], v0);
+            atomicAdd(&a.totals[1], v1);
+            atomicAdd(&a.totals[2], v2);
+            atomicAdd(&a.totals[3], v3);
+        }
+    }
+}
+
+}  // namespace
+}  // namespace ghn
