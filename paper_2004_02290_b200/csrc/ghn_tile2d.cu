@@ -41,7 +41,7 @@ constexpr int T2_SMALL = 4;      // boundary candidates ordered exactly
 constexpr int T2_NL = 4;         // distinct labels tracked by the vote
 constexpr int T2_CAP = 4096;     // staged points per tile
 constexpr int TT_KMAX = 32;      // thread-per-query kernel: largest k
-constexpr double TT_Q = 384.0;   // thread-per-query kernel: queries per tile
+constexpr double TT_Q = 256.0;   // thread-per-query kernel: queries per tile
 constexpr double TT_CAP = 8192.0;
 #ifndef T2_EXT_MAXK
 #define T2_EXT_MAXK 16     // k at or below which phase-1 selects extract
@@ -603,6 +603,7 @@ __device__ __forceinline__ bool shell_cannot_change(const T2Args &a, double q0, 
 // block(l) is (q's distance to its own cell's nearest face) + l * w per axis.
 struct ShellBound {
     double f0, f1, margin;
+    __device__ __forceinline__ ShellBound() : f0(0.0), f1(0.0), margin(0.0) {}
     __device__ __forceinline__ ShellBound(const T2Args &a, double q0, double q1, int64_t cc0, int64_t cc1) {
         f0 = fmin(q0 - (double)(a.lo0 + cc0) * a.w0, (double)(a.lo0 + cc0 + 1) * a.w0 - q0);
         f1 = fmin(q1 - (double)(a.lo1 + cc1) * a.w1, (double)(a.lo1 + cc1 + 1) * a.w1 - q1);
@@ -1260,19 +1261,20 @@ int32_t tile2d_run(const ghn_index_view *ix, const Tile2dPlan *plan, const void 
         int lk = 0;
         while ((1 << lk) < k) ++lk;
         ki = 4 + 2 * lk + (stats ? 1 : 0);
-        static const void *const thr_fns[12] = {
+        static const void *const thr_fns[14] = {
             (const void *)tile2d_thr_kernel<1, false>,  (const void *)tile2d_thr_kernel<1, true>,
             (const void *)tile2d_thr_kernel<2, false>,  (const void *)tile2d_thr_kernel<2, true>,
             (const void *)tile2d_thr_kernel<4, false>,  (const void *)tile2d_thr_kernel<4, true>,
             (const void *)tile2d_thr_kernel<8, false>,  (const void *)tile2d_thr_kernel<8, true>,
             (const void *)tile2d_thr_kernel<16, false>, (const void *)tile2d_thr_kernel<16, true>,
-            (const void *)tile2d_thr_kernel<32, false>, (const void *)tile2d_thr_kernel<32, true>};
+            (const void *)tile2d_thr_kernel<32, false>, (const void *)tile2d_thr_kernel<32, true>,
+            (const void *)tile2d_thr_kernel<64, false>, (const void *)tile2d_thr_kernel<64, true>};
         fn = thr_fns[ki - 4];
     }
     // largest dynamic smem opted into, per device and kernel (function
     // attributes are per device; callers may run on several devices / threads)
     static std::mutex attr_mu;
-    static size_t attr_smem[64][16] = {};
+    static size_t attr_smem[64][20] = {};
     int dev = 0;
     GHN_CUDA_CHECK(cudaGetDevice(&dev));
     std::lock_guard<std::mutex> attr_lock(attr_mu);

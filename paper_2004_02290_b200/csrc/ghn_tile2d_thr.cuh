@@ -126,7 +126,51 @@ struct ThrTotals {
     unsigned long long layers, cells, points, n;
 };
 
-// One query on one thread.  False = sent to the generic kernel.
+// Vote over the list's first k entries (predict.py:29-36).  False = the
+// tie-break needs exact keys (generic kernel).
+template <int KM>
+__device__ __forceinline__ bool thr_vote(const uint32_t (&L)[KM + 1], int k, uint32_t lmask, int &wl, int &top) {
+    uint64_t cn = 0;   // 8-bit counter per label code
+#pragma unroll
+    for (int j = 0; j < KM; ++j)
+        if (j < k) cn += 1ull << (8 * (L[j] & lmask));
+    int ntie = 0;
+    top = 0;
+    wl = 0;
+    for (int lab = 0; lab <= (int)lmask; ++lab) {
+        const int c = (int)((cn >> (8 * lab)) & 0xffu);
+        if (c > top) {
+            top = c;
+            wl = lab;
+            ntie = 1;
+        } else if (c == top && c > 0) {
+            ++ntie;
+        }
+    }
+    if (ntie > 1) {
+        // the tied label of the member minimising (sqrt(key), index): the
+        // first tied entry of the list, provided the first tied entry of
+        // another label is >= 2 d-units behind it (then its key, and its
+        // sqrt, is strictly larger)
+        uint32_t w1 = TT_INF, w2 = TT_INF;
+#pragma unroll
+        for (int j = 0; j < KM; ++j) {
+            const uint32_t lab = L[j] & lmask;
+            const bool tied = j < k && (int)((cn >> (8 * lab)) & 0xffu) == top;
+            if (tied && w1 == TT_INF) w1 = L[j];
+            else if (tied && w2 == TT_INF && lab != (w1 & lmask)) w2 = L[j];
+        }
+        const int lb = __popc(lmask);
+        if ((w2 >> lb) - (w1 >> lb) < 2u) return false;
+        wl = (int)(w1 & lmask);
+    }
+    return true;
+}
+
+// One query on one thread, each lane on its own (no lock-step): the best
+// shape for k <= 4, where the bubble is short and lanes that need more
+// layers should not hold the warp (measured: k = 1 / 4 faster than the
+// lock-step rounds below, k = 16 slower).
 template <int KM, bool STATS>
 __device__ __forceinline__ void process_query_thr(const T2Args &a, const ThrWin &w, int32_t qi, int t0, int t1,
                                                   int r_lo, int c_lo, ThrTotals &tot) {
@@ -270,6 +314,278 @@ __device__ __forceinline__ void process_query_thr(const T2Args &a, const ThrWin 
     }
 }
 
+// Per-range lower bound: q's distance to its own cell's faces (lower / upper
+// per axis) and the rounding margin of ShellBound.  A rectangle of cells at
+// offsets [ra, rb] x [ca, cb] from q's cell cannot hold a point whose key
+// precedes `upper` when its distance to q (less the margin per axis) says so.
+struct RectBound {
+    double fl0, fh0, fl1, fh1, margin;
+    __device__ __forceinline__ RectBound() : fl0(0.0), fh0(0.0), fl1(0.0), fh1(0.0), margin(0.0) {}
+    __device__ __forceinline__ RectBound(const T2Args &a, double q0, double q1, int64_t cc0, int64_t cc1) {
+        fl0 = q0 - (double)(a.lo0 + cc0) * a.w0;
+        fh0 = (double)(a.lo0 + cc0 + 1) * a.w0 - q0;
+        fl1 = q1 - (double)(a.lo1 + cc1) * a.w1;
+        fh1 = (double)(a.lo1 + cc1 + 1) * a.w1 - q1;
+        margin = 1e-9 * fmax(a.w0, a.w1) + 1e-12 * (fabs(q0) + fabs(q1));
+    }
+    __device__ __forceinline__ bool beyond(const T2Args &a, int ra, int rb, int ca, int cb, double upper) const {
+        double dx = ra > 0 ? fh0 + (double)(ra - 1) * a.w0 : (rb < 0 ? fl0 + (double)(-rb - 1) * a.w0 : 0.0);
+        double dy = ca > 0 ? fh1 + (double)(ca - 1) * a.w1 : (cb < 0 ? fl1 + (double)(-cb - 1) * a.w1 : 0.0);
+        dx = fmax(dx - margin, 0.0);
+        dy = fmax(dy - margin, 0.0);
+        return (dx * dx + dy * dy) * (1.0 - 1e-9) > upper;
+    }
+};
+
+// Range r of shell(l), l >= 1, as offsets from q's cell: rows [ra, rb] x cols [ca, cb].
+__device__ __forceinline__ void thr_shell_rect(int l, int r, int &ra, int &rb, int &ca, int &cb) {
+    if (r < 2) {
+        ra = rb = r == 0 ? -l : l;
+        ca = -l;
+        cb = l;
+    } else {
+        ra = rb = -l + 1 + ((r - 2) >> 1);
+        ca = cb = ((r - 2) & 1) ? l : -l;
+    }
+}
+
+// Staged slot range of the cells at offsets (row ra, cols [ca, cb]) from (lr, lc), clipped.
+__device__ __forceinline__ void thr_rect_slots(const ThrWin &w, int lr, int lc, int ra, int ca, int cb, int &s, int &e) {
+    const int row = lr + ra, c0 = max(lc + ca, 0), c1 = min(lc + cb, w.W - 1);
+    s = e = 0;
+    if (row >= 0 && row < w.R && c0 <= c1) {
+        const int32_t *rp = w.loc + row * w.W1;
+        s = rp[c0];
+        e = rp[c1 + 1];
+    }
+}
+
+// The tile's queries in rounds of one query per thread.  Per round:
+//  A  (per lane) load the query; l* = the first layer whose block holds k
+//     points (explore.py: every earlier layer leaves the buffer short, so it
+//     `changed` and no stop rule applies -- T_l* = top-k of block(l*));
+//  B  (warp lock-step) all candidates of block(l*), row by row, into the
+//     list: one candidate per lane per step (+inf pads the shorter lanes), so
+//     the bubble is always issued for the whole warp;
+//  C  (warp lock-step) later layers while some lane continues: each lane
+//     scans its shell's ranges that are not provably beyond the k-th key
+//     (compare only); a lane whose shell changed the top-k re-scans it into
+//     the list;
+//  D  the vote (predict.py:29-36) and the outputs.
+template <int KM, bool STATS>
+__device__ __forceinline__ void run_rounds_thr(const T2Args &a, const ThrWin &w, int qb, int qe, int t0, int t1,
+                                               int r_lo, int c_lo, ThrTotals &tot) {
+    const int k = a.k;
+    const uint32_t lmask = (uint32_t)a.lmask;
+    const int64_t tr0 = (int64_t)t0 * a.T, tc0 = (int64_t)t1 * a.T;
+    for (int base = qb; base < qe; base += TT_THREADS) {
+        const int qq = base + (int)threadIdx.x;
+        bool live = qq < qe;   // this lane holds a query still being answered
+        int32_t qi = 0;
+        double q0 = 0.0, q1 = 0.0;
+        int64_t cc0 = 0, cc1 = 0;
+        int lr = 0, lc = 0, lmax = 0, l = 0, cnt = 0;
+        if (live) {
+            qi = a.qorder[qq];
+            if (a.q_dtype == GHN_F32) {
+                const float2 qf = ((const float2 *)a.Q)[qi];
+                q0 = (double)qf.x;
+                q1 = (double)qf.y;
+            } else {
+                q0 = ((const double *)a.Q)[2 * (int64_t)qi];
+                q1 = ((const double *)a.Q)[2 * (int64_t)qi + 1];
+            }
+            cc0 = cell_id(q0, a.w0, a.inv0, a.pow2 & 1u) - a.lo0;
+            cc1 = cell_id(q1, a.w1, a.inv1, (a.pow2 >> 1) & 1u) - a.lo1;
+            if (cc0 < tr0 || cc0 >= tr0 + a.T || cc1 < tc0 || cc1 >= tc0 + a.T || cc0 >= a.ext0 ||
+                cc1 >= a.ext1) {
+                push_fallback(a, qi);   // centre outside the grid
+                live = false;
+            }
+        }
+        if (live) {
+            lr = (int)(cc0 - r_lo);
+            lc = (int)(cc1 - c_lo);
+            lmax = max(max((int)cc0, a.ext0 - 1 - (int)cc0), max((int)cc1, a.ext1 - 1 - (int)cc1));
+            // l*: block(l) = block(l-1) + shell(l)
+            for (;;) {
+                if (l > a.A) {
+                    push_fallback(a, qi);
+                    live = false;
+                    break;
+                }
+                if (l == 0) {
+                    int s, e;
+                    thr_rect_slots(w, lr, lc, 0, 0, 0, s, e);
+                    cnt = e - s;
+                } else {
+                    for (int r = 0; r < 4 * l; ++r) {
+                        int ra, rb, ca, cb, s, e;
+                        thr_shell_rect(l, r, ra, rb, ca, cb);
+                        thr_rect_slots(w, lr, lc, ra, ca, cb, s, e);
+                        cnt += e - s;
+                    }
+                }
+                if (cnt >= k || l >= lmax) break;
+                ++l;
+            }
+        }
+        // ---- B: block(l) row by row, lock-step
+        uint32_t L[KM + 1];
+#pragma unroll
+        for (int j = 0; j <= KM; ++j) L[j] = TT_INF;
+        {
+            const int n = live ? cnt : 0;
+            const int steps = __reduce_max_sync(GHN_FULL, n);
+            int ra = -l, p = 0, e = 0;
+            if (live) thr_rect_slots(w, lr, lc, ra, -l, l, p, e);
+            for (int it = 0; it < steps; ++it) {
+                const bool have = it < n;
+                while (have && p >= e) {
+                    ++ra;
+                    thr_rect_slots(w, lr, lc, ra, -l, l, p, e);
+                }
+                const int pp = have ? p : 0;
+                uint32_t pk = thr_pack(w.xy[pp], q0, q1, (uint32_t)w.sl[pp], lmask);
+                pk = have ? pk : TT_INF;
+                thr_bubble(L, pk);
+                p += have ? 1 : 0;
+            }
+        }
+        int layers = l;
+        int64_t points = cnt;
+        // stop rules after layer l* (it filled the buffer: changed)
+        if (live && cnt >= k && a.mode == GHN_MODE_GUARANTEED) {
+            const double b = __dmul_rn((double)l, a.min_w);
+            const double b2 = __dmul_rn(b, b);
+            const uint32_t tk = thr_pick(L, k - 1) & ~lmask;
+            if (b2 >= thr_upper(tk, lmask)) {
+                lmax = l;   // stop
+            } else if (b2 > thr_lower(tk)) {
+                push_fallback(a, qi);
+                live = false;
+            }
+        }
+        bool more = live && l < lmax;   // continues with layer l + 1
+        bool fin = live && !more;       // answered after layer l
+        // ---- C: later layers
+        const RectBound rb0 = more ? RectBound(a, q0, q1, cc0, cc1) : RectBound();
+        while (__any_sync(GHN_FULL, more)) {
+            uint32_t tm = 0;
+            double upper = 0.0;
+            if (more) {
+                ++l;
+                if (l > a.A) {
+                    push_fallback(a, qi);
+                    more = false;
+                }
+                tm = thr_pick(L, k - 1) & ~lmask;
+                upper = thr_upper(tm, lmask);
+            }
+            // compare-only scan of the shell's ranges that may hold a point preceding the k-th
+            bool lt = false, eq = false;
+            int sc = 0;   // points of shell(l) (stats)
+            {
+                int r = 0, p = 0, e = 0;
+                const int nr = 4 * l;
+                bool act = more;
+                for (;;) {
+                    while (act && p >= e) {
+                        if (r >= nr) {
+                            act = false;
+                            break;
+                        }
+                        int ra, rb, ca, cb;
+                        thr_shell_rect(l, r, ra, rb, ca, cb);
+                        ++r;
+                        thr_rect_slots(w, lr, lc, ra, ca, cb, p, e);
+                        if (STATS) sc += e - p;
+                        if (rb0.beyond(a, ra, rb, ca, cb, upper)) e = p;
+                    }
+                    if (!__any_sync(GHN_FULL, act)) break;
+                    const int pp = act ? p : 0;
+                    const uint32_t pk = thr_pack(w.xy[pp], q0, q1, (uint32_t)w.sl[pp], lmask);
+                    lt |= act && pk < tm;
+                    eq |= act && (uint32_t)(pk - tm) <= lmask;
+                    p += act ? 1 : 0;
+                }
+            }
+            if (more && eq) {   // a shell point shares the k-th key's d-part
+                push_fallback(a, qi);
+                more = false;
+            }
+            // a lane whose shell changed the top-k brings the shell into the list
+            bool redo = more && lt;
+            if (__any_sync(GHN_FULL, redo)) {
+                int r = 0, p = 0, e = 0;
+                const int nr = 4 * l;
+                for (;;) {
+                    while (redo && p >= e) {
+                        if (r >= nr) {
+                            redo = false;
+                            break;
+                        }
+                        int ra, rb, ca, cb;
+                        thr_shell_rect(l, r, ra, rb, ca, cb);
+                        ++r;
+                        thr_rect_slots(w, lr, lc, ra, ca, cb, p, e);
+                        if (rb0.beyond(a, ra, rb, ca, cb, upper)) e = p;
+                    }
+                    if (!__any_sync(GHN_FULL, redo)) break;
+                    const int pp = redo ? p : 0;
+                    uint32_t pk = thr_pack(w.xy[pp], q0, q1, (uint32_t)w.sl[pp], lmask);
+                    pk = redo ? pk : TT_INF;
+                    thr_bubble(L, pk);
+                    p += redo ? 1 : 0;
+                }
+            }
+            if (more) {
+                layers = l;
+                points += sc;
+                bool stop = !lt && a.mode == GHN_MODE_HEURISTIC;
+                if (a.mode == GHN_MODE_GUARANTEED) {
+                    const double b = __dmul_rn((double)l, a.min_w);
+                    const double b2 = __dmul_rn(b, b);
+                    const uint32_t tk = thr_pick(L, k - 1) & ~lmask;
+                    if (b2 >= thr_upper(tk, lmask)) {
+                        stop = true;
+                    } else if (b2 > thr_lower(tk)) {
+                        push_fallback(a, qi);
+                        more = false;
+                    }
+                }
+                if (more && (stop || l >= lmax)) {
+                    more = false;
+                    fin = true;
+                }
+            }
+        }
+        // ---- D: vote and outputs
+        if (fin) {
+            const uint32_t tau = thr_pick(L, k - 1), nx = thr_pick(L, k);
+            int wl, top;
+            if ((nx != TT_INF && (nx & ~lmask) == (tau & ~lmask)) || !thr_vote<KM>(L, k, lmask, wl, top)) {
+                push_fallback(a, qi);
+            } else {
+                if (a.out_label) a.out_label[qi] = wl;
+                if (a.out_conf) a.out_conf[qi] = __ddiv_rn((double)top, (double)k);
+                if (STATS) {
+                    const int cells = thr_block_cells(w, lr, lc, layers);
+                    if (a.out_stats) {
+                        a.out_stats[3 * (int64_t)qi + 0] = layers;
+                        a.out_stats[3 * (int64_t)qi + 1] = cells;
+                        a.out_stats[3 * (int64_t)qi + 2] = points;
+                    }
+                    tot.layers += layers;
+                    tot.cells += cells;
+                    tot.points += points;
+                    tot.n += 1;
+                }
+            }
+        }
+    }
+}
+
 template <int KM, bool STATS>
 __global__ void __launch_bounds__(TT_THREADS) tile2d_thr_kernel(const T2Args a) {
     extern __shared__ __align__(16) unsigned char sm[];
@@ -325,8 +641,12 @@ __global__ void __launch_bounds__(TT_THREADS) tile2d_thr_kernel(const T2Args a) 
     __syncthreads();
     const ThrWin w{sxy, sl, loc, R, W, W1};
     ThrTotals tot{0, 0, 0, 0};
-    for (int qq = qb + (int)threadIdx.x; qq < qe; qq += TT_THREADS)
-        process_query_thr<KM, STATS>(a, w, a.qorder[qq], t0, t1, r_lo, c_lo, tot);
+    if (KM <= 4) {
+        for (int qq = qb + (int)threadIdx.x; qq < qe; qq += TT_THREADS)
+            process_query_thr<KM, STATS>(a, w, a.qorder[qq], t0, t1, r_lo, c_lo, tot);
+    } else {
+        run_rounds_thr<KM, STATS>(a, w, qb, qe, t0, t1, r_lo, c_lo, tot);
+    }
     if (STATS && a.totals) {
         const unsigned long long v0 = warp_sum(tot.layers), v1 = warp_sum(tot.cells), v2 = warp_sum(tot.points),
                                  v3 = warp_sum(tot.n);
