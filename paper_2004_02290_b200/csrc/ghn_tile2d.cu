@@ -40,7 +40,8 @@ constexpr int T2_NB = 32;        // histogram buckets per select round
 constexpr int T2_SMALL = 4;      // boundary candidates ordered exactly
 constexpr int T2_NL = 4;         // distinct labels tracked by the vote
 constexpr int T2_CAP = 4096;     // staged points per tile
-constexpr int TT_KMAX = 32;      // thread-per-query kernel: largest k
+constexpr int TT_KMAX = 255;     // thread-per-query kernel: largest k (8-bit vote counters)
+constexpr int TT_LIST_KMAX = 32; // largest k on the register list; above: bucket select
 constexpr double TT_Q = 256.0;   // thread-per-query kernel: queries per tile
 constexpr double TT_CAP = 8192.0;
 #ifndef T2_EXT_MAXK
@@ -77,6 +78,7 @@ struct T2Args {
     int32_t dbg;
     int32_t small_labels;
     int32_t lmask;   // label-code mask of the thread kernel (2^LB - 1)
+    int32_t sb_capn, sb_redo, sb_wmax;   // bucket-select lock-step limits (see ghn_tile2d_thr.cuh)
 };
 
 struct Win {
@@ -1105,6 +1107,13 @@ __global__ void window_density_kernel(const int32_t *__restrict__ cell_start, co
 
 }  // namespace
 
+// Largest k answered with the register list; larger k use the bucket select
+// (GHN_TT_LISTMAX overrides, for measurements).
+static int tt_list_kmax() {
+    static const int v = getenv("GHN_TT_LISTMAX") ? atoi(getenv("GHN_TT_LISTMAX")) : TT_LIST_KMAX;
+    return v;
+}
+
 bool tile2d_plan(const ghn_index_view *ix, int64_t nq, int32_t k, int32_t task, bool want_neighbors,
                  Tile2dPlan *plan) {
     memset(plan, 0, sizeof(*plan));
@@ -1167,6 +1176,7 @@ bool tile2d_plan(const ghn_index_view *ix, int64_t nq, int32_t k, int32_t task, 
     if (plan->G == 1) {   // float2 coordinates + u8 label code per staged point
         plan->smem = (size_t)cap * 9 + (size_t)plan->win * (plan->win + 1) * 4 + (size_t)plan->win * 4 +
                      (size_t)(plan->win + 1) * 4 + 64;
+        if (k > tt_list_kmax()) plan->smem += (size_t)SB_NB * TT_THREADS;   // bucket select: byte histograms
         return plan->smem <= 200 * 1024;
     }
     // the warp kernel also stages each point's index (int32) and label code (u8)
@@ -1250,6 +1260,9 @@ int32_t tile2d_run(const ghn_index_view *ix, const Tile2dPlan *plan, const void 
     a.dbg = getenv("GHN_DEBUG_MODE") ? atoi(getenv("GHN_DEBUG_MODE")) : 0;
     a.small_labels = ix->n_labels > 0 && ix->n_labels <= 32;
     a.lmask = ix->n_labels <= 2 ? 1 : (ix->n_labels <= 4 ? 3 : 7);
+    a.sb_capn = getenv("GHN_SB_CAPN") ? atoi(getenv("GHN_SB_CAPN")) : 255;
+    a.sb_redo = getenv("GHN_SB_REDO") ? atoi(getenv("GHN_SB_REDO")) : 2;
+    a.sb_wmax = getenv("GHN_SB_WMAX") ? atoi(getenv("GHN_SB_WMAX")) : 0;
     const bool stats = out->stats != nullptr || out->totals != nullptr;
     // warp kernel: extraction select for small k (EXT), histogram select otherwise
     int ki = plan->G == 8 ? 1 : (plan->G == 16 ? 2 : (k >= 2 && k <= T2_EXT_MAXK ? 3 : 0));
@@ -1257,18 +1270,19 @@ int32_t tile2d_run(const ghn_index_view *ix, const Tile2dPlan *plan, const void 
                      : ki == 3 ? (const void *)tile2d_kernel<true>
                      : ki == 1 ? (const void *)tile2d_grp_kernel<8>
                                : (const void *)tile2d_grp_kernel<16>;
-    if (plan->G == 1) {   // thread per query: list capacity KM = next power of two >= k
+    if (plan->G == 1) {   // thread per query: list capacity KM = next power of two >= k; 0 = bucket select
         int lk = 0;
         while ((1 << lk) < k) ++lk;
-        ki = 4 + 2 * lk + (stats ? 1 : 0);
+        const int v = k > tt_list_kmax() ? 0 : lk + 1;
+        ki = 4 + 2 * v + (stats ? 1 : 0);
         static const void *const thr_fns[14] = {
+            (const void *)tile2d_thr_kernel<0, false>,  (const void *)tile2d_thr_kernel<0, true>,
             (const void *)tile2d_thr_kernel<1, false>,  (const void *)tile2d_thr_kernel<1, true>,
             (const void *)tile2d_thr_kernel<2, false>,  (const void *)tile2d_thr_kernel<2, true>,
             (const void *)tile2d_thr_kernel<4, false>,  (const void *)tile2d_thr_kernel<4, true>,
             (const void *)tile2d_thr_kernel<8, false>,  (const void *)tile2d_thr_kernel<8, true>,
             (const void *)tile2d_thr_kernel<16, false>, (const void *)tile2d_thr_kernel<16, true>,
-            (const void *)tile2d_thr_kernel<32, false>, (const void *)tile2d_thr_kernel<32, true>,
-            (const void *)tile2d_thr_kernel<64, false>, (const void *)tile2d_thr_kernel<64, true>};
+            (const void *)tile2d_thr_kernel<32, false>, (const void *)tile2d_thr_kernel<32, true>};
         fn = thr_fns[ki - 4];
     }
     // largest dynamic smem opted into, per device and kernel (function

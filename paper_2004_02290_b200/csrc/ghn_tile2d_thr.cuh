@@ -586,6 +586,397 @@ __device__ __forceinline__ void run_rounds_thr(const T2Args &a, const ThrWin &w,
     }
 }
 
+// ---------------------------------------------------------------- k > 32
+// Bucket select (k in (32, 255]): the bubble's cost grows with k, so for
+// large k block(l*) is passed over twice in lock-step.  Pass 1 histograms
+// the packed keys into SB_NB buckets of 1/16 octave (packed >> 17: exponent
+// and 4 mantissa bits -- bucket edges are d-part edges) around the expected
+// k-th key, in a per-lane byte histogram in shared memory; the bucket bb
+// where the count reaches k follows.  Pass 2 votes every candidate below bb
+// and bubbles the bucket-bb candidates into a list of SB_C + 1: the k-th is
+// its r-th entry (r = k - count below bb).  Later shells are checked
+// compare-only; a later layer that changes the top-k, a boundary bucket
+// holding the k-th beyond SB_C, or a wrapped byte counter sends the
+// query to the generic kernel.  Byte counters may wrap beyond 255 points in
+// one bucket: pass 2 recounts the buckets up to bb and falls back on a
+// mismatch.
+constexpr int SB_NB = 64;   // buckets (0 and SB_NB-1 catch the tails)
+constexpr int SB_S = 17;    // packed >> SB_S: 16 buckets per octave
+constexpr int SB_C = 8;     // boundary list capacity
+constexpr int SB_REDO = 8;  // fewest lanes of a warp re-selecting over a larger block
+
+__device__ __forceinline__ int sb_bucket(uint32_t pk, int bbase) {
+    return min(max((int)(pk >> SB_S) - bbase, 0), SB_NB - 1);
+}
+
+template <bool STATS>
+__device__ __forceinline__ void run_rounds_sel(const T2Args &a, const ThrWin &w, uint32_t *hist, int qb, int qe,
+                                               int t0, int t1, int r_lo, int c_lo, ThrTotals &tot) {
+    const int k = a.k;
+    const uint32_t lmask = (uint32_t)a.lmask;
+    const uint32_t fmask = 2u * lmask + 1u;   // label bits + the shell flag above them
+    const int64_t tr0 = (int64_t)t0 * a.T, tc0 = (int64_t)t1 * a.T;
+    uint32_t *myh = hist + threadIdx.x;   // word i of this lane at myh[i * TT_THREADS]
+    for (int base = qb; base < qe; base += TT_THREADS) {
+        const int qq = base + (int)threadIdx.x;
+        bool live = qq < qe;
+        int32_t qi = 0;
+        double q0 = 0.0, q1 = 0.0;
+        int64_t cc0 = 0, cc1 = 0;
+        int lr = 0, lc = 0, lmax = 0, l = 0, cnt = 0;
+        if (live) {
+            qi = a.qorder[qq];
+            if (a.q_dtype == GHN_F32) {
+                const float2 qf = ((const float2 *)a.Q)[qi];
+                q0 = (double)qf.x;
+                q1 = (double)qf.y;
+            } else {
+                q0 = ((const double *)a.Q)[2 * (int64_t)qi];
+                q1 = ((const double *)a.Q)[2 * (int64_t)qi + 1];
+            }
+            cc0 = cell_id(q0, a.w0, a.inv0, a.pow2 & 1u) - a.lo0;
+            cc1 = cell_id(q1, a.w1, a.inv1, (a.pow2 >> 1) & 1u) - a.lo1;
+            if (cc0 < tr0 || cc0 >= tr0 + a.T || cc1 < tc0 || cc1 >= tc0 + a.T || cc0 >= a.ext0 ||
+                cc1 >= a.ext1) {
+                push_fallback(a, qi);
+                live = false;
+            }
+        }
+        if (live) {
+            lr = (int)(cc0 - r_lo);
+            lc = (int)(cc1 - c_lo);
+            lmax = max(max((int)cc0, a.ext0 - 1 - (int)cc0), max((int)cc1, a.ext1 - 1 - (int)cc1));
+            for (;;) {
+                if (l > a.A) {
+                    push_fallback(a, qi);
+                    live = false;
+                    break;
+                }
+                if (l == 0) {
+                    int s, e;
+                    thr_rect_slots(w, lr, lc, 0, 0, 0, s, e);
+                    cnt = e - s;
+                } else {
+                    for (int r = 0; r < 4 * l; ++r) {
+                        int ra, rb, ca, cb, s, e;
+                        thr_shell_rect(l, r, ra, rb, ca, cb);
+                        thr_rect_slots(w, lr, lc, ra, ca, cb, s, e);
+                        cnt += e - s;
+                    }
+                }
+                if (cnt >= k || l >= lmax) break;
+                ++l;
+            }
+        }
+        // Select over block(ls) (lock-step passes), then check the later
+        // shells compare-only; a shell that changes the top-k makes its
+        // block the next select (explore.py:104-130).
+        int ls = l, layers = l, cls = 0;
+        bool need = live, fin = false;
+        // Heuristic mode, l* barely full (expected k-th radius beyond 0.8 of
+        // the block's half-width): shell(l*+1) will most likely change the
+        // top-k, so select over block(l*+1) at once and learn changed(l*+1)
+        // from a flag on the shell's candidates (T_{l*+1} holds one of them).
+        // Only when block(l*+1) adds no lock-step steps (the warp's largest
+        // block(l*) holds at least as many points).
+        bool skipm = false;
+        const int wmax = __reduce_max_sync(GHN_FULL, live ? cnt : 0);
+        if (live && a.mode == GHN_MODE_HEURISTIC && l < lmax && l + 1 <= a.A) {
+            const double kc = (double)k * (2.0 * l + 1.0) * (2.0 * l + 1.0) / (3.14159265358979 * (double)cnt);
+            const double fc = 0.8 * ((double)l + 0.5);
+            if (kc > fc * fc) {
+                int sc = 0;
+                for (int r = 0; r < 4 * (l + 1); ++r) {
+                    int ra, rb, ca, cb, s0, e0;
+                    thr_shell_rect(l + 1, r, ra, rb, ca, cb);
+                    thr_rect_slots(w, lr, lc, ra, ca, cb, s0, e0);
+                    sc += e0 - s0;
+                }
+                if (cnt + sc <= (a.sb_wmax ? wmax : a.sb_capn)) {
+                    skipm = true;
+                    ls = l + 1;
+                    cnt += sc;
+                }
+            }
+        }
+        uint64_t cn = 0;
+        uint32_t tau = 0, tm = 0;
+        double upper = 0.0;
+        const RectBound rb0 = live ? RectBound(a, q0, q1, cc0, cc1) : RectBound();
+        while (__any_sync(GHN_FULL, need)) {
+            // expected k-th key from the block's density: buckets cover [K/4, ~4K)
+            int bbase = 0;
+            if (need) {
+                const double side = (double)(2 * ls + 1);
+                const double kest = (double)k * side * side * a.w0 * a.w1 / (3.14159265358979 * (double)cnt);
+                const double klo = kest * 0.25;
+                const uint32_t top = __funnelshift_l((uint32_t)__double2loint(klo), (uint32_t)__double2hiint(klo), 1);
+                bbase = (int)(top >> SB_S) - 1;
+            }
+#pragma unroll
+            for (int i = 0; i < SB_NB / 4; ++i) myh[i * TT_THREADS] = 0u;
+            const int n = need ? cnt : 0;
+            const int steps = __reduce_max_sync(GHN_FULL, n);
+            // ---- pass 1: histogram
+            {
+                int ra = -ls, p = 0, e = 0;
+                if (need) thr_rect_slots(w, lr, lc, ra, -ls, ls, p, e);
+                for (int it = 0; it < steps; ++it) {
+                    const bool have = it < n;
+                    while (have && p >= e) {
+                        ++ra;
+                        thr_rect_slots(w, lr, lc, ra, -ls, ls, p, e);
+                    }
+                    if (have) {
+                        const int b = sb_bucket(thr_pack(w.xy[p], q0, q1, 0u, fmask), bbase);
+                        myh[(b >> 2) * TT_THREADS] += 1u << (8 * (b & 3));
+                    }
+                    p += have ? 1 : 0;
+                }
+            }
+            int bb = 0, below = 0, nbb = 0;
+            bool sel = need;
+            if (sel) {   // the bucket where the running count reaches k
+                int cum = 0;
+                bool found = false;
+                for (int i = 0; i < SB_NB / 4 && !found; ++i) {
+                    const uint32_t wd = myh[i * TT_THREADS];
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const int c = (int)((wd >> (8 * j)) & 0xffu);
+                        if (!found && cum + c >= k) {
+                            bb = 4 * i + j;
+                            below = cum;
+                            nbb = c;
+                            found = true;
+                        }
+                        cum += c;
+                    }
+                }
+                if (!found || k - below > SB_C) {   // wrapped counts, or the k-th too deep in its bucket
+                    push_fallback(a, qi);
+                    sel = false;
+                }
+            }
+            // ---- pass 2: vote below bb, list of the bucket-bb candidates
+            uint32_t Lb[SB_C + 1];
+#pragma unroll
+            for (int j = 0; j <= SB_C; ++j) Lb[j] = TT_INF;
+            if (sel) cn = 0;
+            bool chg = false;   // a shell(ls) candidate below the boundary bucket (skip mode)
+            int nlo = 0, neq = 0;   // recount of the histogram up to bb (byte counters may wrap)
+            {
+                int ra = -ls, p = 0, e = 0, pi0 = 0, pi1 = 0;
+                if (sel) {
+                    thr_rect_slots(w, lr, lc, ra, -ls, ls, p, e);
+                    thr_rect_slots(w, lr, lc, ra, -(ls - 1), ls - 1, pi0, pi1);
+                }
+                for (int it = 0; it < steps; ++it) {
+                    const bool have = sel && it < n;
+                    while (have && p >= e) {
+                        ++ra;
+                        thr_rect_slots(w, lr, lc, ra, -ls, ls, p, e);
+                        thr_rect_slots(w, lr, lc, ra, -(ls - 1), ls - 1, pi0, pi1);
+                    }
+                    const int pp = have ? p : 0;
+                    const bool insh = skipm && (ra == -ls || ra == ls || pp < pi0 || pp >= pi1);
+                    const uint32_t pk =
+                        thr_pack(w.xy[pp], q0, q1, (uint32_t)w.sl[pp] | (insh ? lmask + 1u : 0u), fmask);
+                    const int b = sb_bucket(pk, bbase);
+                    if (have && b < bb) {
+                        cn += 1ull << (8 * (pk & lmask));
+                        chg |= insh;
+                        ++nlo;
+                    }
+                    neq += have && b == bb ? 1 : 0;
+                    thr_bubble(Lb, have && b == bb ? pk : TT_INF);
+                    p += have ? 1 : 0;
+                }
+            }
+            need = false;
+            bool more = false;
+            if (sel) {
+                const int r = k - below;
+                tau = thr_pick(Lb, r - 1);
+                const uint32_t nx = r < nbb ? thr_pick(Lb, r) : TT_INF;
+                bool stop = false, bad = false;
+                tm = tau & ~fmask;
+                upper = thr_upper(tm, fmask);
+#pragma unroll
+                for (int j = 0; j < SB_C; ++j)
+                    if (j < r) {
+                        cn += 1ull << (8 * (Lb[j] & lmask));
+                        chg |= (Lb[j] & (lmask + 1u)) != 0u;
+                    }
+                l = layers = ls;
+                cls = cnt;
+                if (nlo != below || neq != nbb) bad = true;   // a byte counter wrapped
+                // layer ls filled / changed the buffer, or (skip mode) changed iff a shell member
+                const bool changed = !skipm || chg;
+                skipm = false;
+                stop = !changed;
+                bad |= nx != TT_INF && (nx & ~fmask) == tm;
+                if (!bad && a.mode == GHN_MODE_GUARANTEED) {   // layer ls changed: only the bound may stop
+                    const double b = __dmul_rn((double)l, a.min_w);
+                    const double b2 = __dmul_rn(b, b);
+                    if (b2 >= upper) stop = true;
+                    else if (b2 > thr_lower(tm)) bad = true;
+                }
+                if (bad) push_fallback(a, qi);
+                else if (stop || l >= lmax) fin = true;
+                else more = true;
+            }
+            // ---- later layers, compare-only
+            while (__any_sync(GHN_FULL, more)) {
+                if (more) {
+                    ++l;
+                    if (l > a.A) {
+                        push_fallback(a, qi);
+                        more = false;
+                    }
+                }
+                bool lt = false, eq = false;
+                int sc = 0;   // all points of shell(l)
+                {
+                    int rr = 0, p = 0, e = 0;
+                    const int nr = 4 * l;
+                    bool act = more;
+                    for (;;) {
+                        while (act && p >= e) {
+                            if (rr >= nr) {
+                                act = false;
+                                break;
+                            }
+                            int ra, rb, ca, cb;
+                            thr_shell_rect(l, rr, ra, rb, ca, cb);
+                            ++rr;
+                            thr_rect_slots(w, lr, lc, ra, ca, cb, p, e);
+                            sc += e - p;
+                            if (rb0.beyond(a, ra, rb, ca, cb, upper)) e = p;
+                        }
+                        if (!__any_sync(GHN_FULL, act)) break;
+                        const int pp = act ? p : 0;
+                        const uint32_t pk = thr_pack(w.xy[pp], q0, q1, (uint32_t)w.sl[pp], fmask);
+                        lt |= act && pk < tm;
+                        eq |= act && (uint32_t)(pk - tm) <= fmask;
+                        p += act ? 1 : 0;
+                    }
+                }
+                if (more && eq) {   // undecidable d-part
+                    push_fallback(a, qi);
+                    more = false;
+                }
+                if (more) {
+                    layers = l;
+                    cnt += sc;
+                    if (lt) {   // shell(l) changed the top-k: select over block(l)
+                        more = false;
+                        ls = l;
+                        need = true;
+                    }
+                    if (!lt) {
+                        bool stop = a.mode == GHN_MODE_HEURISTIC;
+                        if (a.mode == GHN_MODE_GUARANTEED) {
+                            const double b = __dmul_rn((double)l, a.min_w);
+                            const double b2 = __dmul_rn(b, b);
+                            if (b2 >= upper) {
+                                stop = true;
+                            } else if (b2 > thr_lower(tm)) {
+                                push_fallback(a, qi);
+                                more = false;
+                            }
+                        }
+                        if (more && (stop || l >= lmax)) {
+                            more = false;
+                            fin = true;
+                        }
+                    }
+                }
+            }
+            // a lone re-select would hold the whole warp for a block's worth
+            // of steps: below SB_REDO lanes the generic kernel is cheaper
+            const int nredo = __popc(__ballot_sync(GHN_FULL, need));
+            if (need && (nredo < a.sb_redo || cnt > a.sb_capn)) {
+                push_fallback(a, qi);
+                need = false;
+            }
+        }
+        const int64_t points = cnt;   // every layer up to `layers` counted in full
+        // ---- vote: top count; a tie is resolved by a third lock-step pass
+        int top = 0, ntie = 0, wl = 0;
+        if (fin) {
+            for (int lab = 0; lab <= (int)lmask; ++lab) {
+                const int c = (int)((cn >> (8 * lab)) & 0xffu);
+                if (c > top) {
+                    top = c;
+                    wl = lab;
+                    ntie = 1;
+                } else if (c == top && c > 0) {
+                    ++ntie;
+                }
+            }
+        }
+        bool tie = fin && ntie > 1;
+        if (__any_sync(GHN_FULL, tie)) {
+            // smallest packed member per label (members: d-part <= the k-th's)
+            uint32_t mn[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) mn[j] = TT_INF;
+            int ra = -ls, p = 0, e = 0;
+            if (tie) thr_rect_slots(w, lr, lc, ra, -ls, ls, p, e);
+            const int n3 = tie ? cls : 0;
+            const int steps3 = __reduce_max_sync(GHN_FULL, n3);
+            for (int it = 0; it < steps3; ++it) {
+                const bool have = it < n3;
+                while (have && p >= e) {
+                    ++ra;
+                    thr_rect_slots(w, lr, lc, ra, -ls, ls, p, e);
+                }
+                const int pp = have ? p : 0;
+                const uint32_t pk = thr_pack(w.xy[pp], q0, q1, (uint32_t)w.sl[pp], fmask);
+                const bool mem = have && (pk & ~fmask) <= tm;
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+                    if (mem && (pk & lmask) == (uint32_t)j) mn[j] = min(mn[j], pk);
+                p += have ? 1 : 0;
+            }
+            if (tie) {
+                uint32_t w1 = TT_INF, w2 = TT_INF;
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+                    if ((int)((cn >> (8 * j)) & 0xffu) == top && j <= (int)lmask) w1 = min(w1, mn[j]);
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+                    if ((int)((cn >> (8 * j)) & 0xffu) == top && j <= (int)lmask && (uint32_t)j != (w1 & lmask))
+                        w2 = min(w2, mn[j]);
+                const int lbits = __popc(fmask);
+                if ((w2 >> lbits) - (w1 >> lbits) < 2u) {
+                    push_fallback(a, qi);
+                    fin = false;
+                } else {
+                    wl = (int)(w1 & lmask);
+                }
+            }
+        }
+        if (fin) {
+            if (a.out_label) a.out_label[qi] = wl;
+            if (a.out_conf) a.out_conf[qi] = __ddiv_rn((double)top, (double)k);
+            if (STATS) {
+                const int cells = thr_block_cells(w, lr, lc, layers);
+                if (a.out_stats) {
+                    a.out_stats[3 * (int64_t)qi + 0] = layers;
+                    a.out_stats[3 * (int64_t)qi + 1] = cells;
+                    a.out_stats[3 * (int64_t)qi + 2] = points;
+                }
+                tot.layers += layers;
+                tot.cells += cells;
+                tot.points += points;
+                tot.n += 1;
+            }
+        }
+    }
+}
+
 template <int KM, bool STATS>
 __global__ void __launch_bounds__(TT_THREADS) tile2d_thr_kernel(const T2Args a) {
     extern __shared__ __align__(16) unsigned char sm[];
@@ -641,7 +1032,9 @@ __global__ void __launch_bounds__(TT_THREADS) tile2d_thr_kernel(const T2Args a) 
     __syncthreads();
     const ThrWin w{sxy, sl, loc, R, W, W1};
     ThrTotals tot{0, 0, 0, 0};
-    if (KM <= 4) {
+    if (KM == 0) {
+        run_rounds_sel<STATS>(a, w, (uint32_t *)(rstart + a.win + 1), qb, qe, t0, t1, r_lo, c_lo, tot);
+    } else if (KM <= 4) {
         for (int qq = qb + (int)threadIdx.x; qq < qe; qq += TT_THREADS)
             process_query_thr<KM, STATS>(a, w, a.qorder[qq], t0, t1, r_lo, c_lo, tot);
     } else {
