@@ -789,7 +789,8 @@ __device__ __forceinline__ void run_rounds_sel(const T2Args &a, const ThrWin &w,
                         ++nlo;
                     }
                     neq += have && b == bb ? 1 : 0;
-                    thr_bubble(Lb, have && b == bb ? pk : TT_INF);
+                    const bool inb = have && b == bb;
+                    if (__any_sync(GHN_FULL, inb)) thr_bubble(Lb, inb ? pk : TT_INF);
                     p += have ? 1 : 0;
                 }
             }
