@@ -463,7 +463,7 @@ def run_ours(args):
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "peak_kind": peak_kind,
                          "traffic": ncu_traffic(cfg, ks),
-                         "kernel": "ghn_query: tile2d_kernel (+ binning, + query_kernel fallbacks); "
+                         "kernel": "ghn_query: tile2d_thr_kernel, thread per query (+ binning, + query_kernel fallbacks); "
                                    "time = whole predict call, not the kernel alone",
                          "algorithmic_bytes_per_step": sum(algo_bytes.values()),
                          "issue_roofline": issue_roofline()},

@@ -15,7 +15,7 @@ def rows(path):
 
 
 def summarize(paths_by_k, src):
-    out = {"source": src, "kernel": "tile2d_kernel / tile2d_grp_kernel (+ query_kernel fallback)",
+    out = {"source": src, "kernel": "tile2d_thr_kernel (k <= 32: register list; k > 32: bucket select) (+ query_kernel fallback)",
            "query_kernel_dram_bytes_per_launch": {}, "ncu_duration_ms": {}, "l2_hit_pct": {},
            "branch_uniformity_pct": {}, "kernels_in_step": {}}
     for k, p in paths_by_k.items():
