@@ -609,12 +609,25 @@ __device__ __forceinline__ int sb_bucket(uint32_t pk, int bbase) {
     return min(max((int)(pk >> SB_S) - bbase, 0), SB_NB - 1);
 }
 
+// The same bucket from an fp32 key (fp32 queries): bucket edges are the same
+// reals (exponent + 4 mantissa bits; the fp64 index = fp32 index + (1023 -
+// 127) * 16).  The fp32 key is within a few ulps of the exact key, so the
+// bucket is exact unless the key lies within 8 ulps of an edge (`edge`).
+constexpr int SB_F32_SHIFT = (1023 - 127) * 16;
+__device__ __forceinline__ int sb_bucket32(float2 c, float q0f, float q1f, int bbase, bool &edge) {
+    const float dx = c.x - q0f, dy = c.y - q1f;
+    const uint32_t bits = __float_as_uint(__fmaf_rn(dy, dy, dx * dx));
+    edge = ((bits + 8u) & 0x7ffffu) < 16u;
+    return min(max((int)(bits >> 19) + SB_F32_SHIFT - bbase, 0), SB_NB - 1);
+}
+
 template <bool STATS>
 __device__ __forceinline__ void run_rounds_sel(const T2Args &a, const ThrWin &w, uint32_t *hist, int qb, int qe,
                                                int t0, int t1, int r_lo, int c_lo, ThrTotals &tot) {
     const int k = a.k;
     const uint32_t lmask = (uint32_t)a.lmask;
     const uint32_t fmask = 2u * lmask + 1u;   // label bits + the shell flag above them
+    const bool f32q = a.q_dtype == GHN_F32;   // fp32 queries: fp32 keys prefilter the buckets
     const int64_t tr0 = (int64_t)t0 * a.T, tc0 = (int64_t)t1 * a.T;
     uint32_t *myh = hist + threadIdx.x;   // word i of this lane at myh[i * TT_THREADS]
     for (int base = qb; base < qe; base += TT_THREADS) {
@@ -622,6 +635,7 @@ __device__ __forceinline__ void run_rounds_sel(const T2Args &a, const ThrWin &w,
         bool live = qq < qe;
         int32_t qi = 0;
         double q0 = 0.0, q1 = 0.0;
+        float q0f = 0.0f, q1f = 0.0f;
         int64_t cc0 = 0, cc1 = 0;
         int lr = 0, lc = 0, lmax = 0, l = 0, cnt = 0;
         if (live) {
@@ -630,6 +644,8 @@ __device__ __forceinline__ void run_rounds_sel(const T2Args &a, const ThrWin &w,
                 const float2 qf = ((const float2 *)a.Q)[qi];
                 q0 = (double)qf.x;
                 q1 = (double)qf.y;
+                q0f = qf.x;
+                q1f = qf.y;
             } else {
                 q0 = ((const double *)a.Q)[2 * (int64_t)qi];
                 q1 = ((const double *)a.Q)[2 * (int64_t)qi + 1];
@@ -727,8 +743,10 @@ __device__ __forceinline__ void run_rounds_sel(const T2Args &a, const ThrWin &w,
                         ++ra;
                         thr_rect_slots(w, lr, lc, ra, -ls, ls, p, e);
                     }
-                    if (have) {
-                        const int b = sb_bucket(thr_pack(w.xy[p], q0, q1, 0u, fmask), bbase);
+                    if (have) {   // approximate buckets are fine here: pass 2 recounts exactly
+                        bool edge;
+                        const int b = f32q ? sb_bucket32(w.xy[p], q0f, q1f, bbase, edge)
+                                           : sb_bucket(thr_pack(w.xy[p], q0, q1, 0u, fmask), bbase);
                         myh[(b >> 2) * TT_THREADS] += 1u << (8 * (b & 3));
                     }
                     p += have ? 1 : 0;
@@ -780,16 +798,16 @@ __device__ __forceinline__ void run_rounds_sel(const T2Args &a, const ThrWin &w,
                     }
                     const int pp = have ? p : 0;
                     const bool insh = skipm && (ra == -ls || ra == ls || pp < pi0 || pp >= pi1);
-                    const uint32_t pk =
-                        thr_pack(w.xy[pp], q0, q1, (uint32_t)w.sl[pp] | (insh ? lmask + 1u : 0u), fmask);
+                    const uint32_t lab = (uint32_t)w.sl[pp] | (insh ? lmask + 1u : 0u);
+                    const uint32_t pk = thr_pack(w.xy[pp], q0, q1, lab, fmask);
                     const int b = sb_bucket(pk, bbase);
                     if (have && b < bb) {
-                        cn += 1ull << (8 * (pk & lmask));
+                        cn += 1ull << (8 * (lab & lmask));
                         chg |= insh;
                         ++nlo;
                     }
-                    neq += have && b == bb ? 1 : 0;
                     const bool inb = have && b == bb;
+                    neq += inb ? 1 : 0;
                     if (__any_sync(GHN_FULL, inb)) thr_bubble(Lb, inb ? pk : TT_INF);
                     p += have ? 1 : 0;
                 }
@@ -797,10 +815,12 @@ __device__ __forceinline__ void run_rounds_sel(const T2Args &a, const ThrWin &w,
             need = false;
             bool more = false;
             if (sel) {
-                const int r = k - below;
-                tau = thr_pick(Lb, r - 1);
-                const uint32_t nx = r < nbb ? thr_pick(Lb, r) : TT_INF;
-                bool stop = false, bad = false;
+                // pass 1 counted approximately (fp32 keys, byte counters that may
+                // wrap): the exact counts of pass 2 must put the k-th in bucket bb
+                const int r = k - nlo;
+                bool stop = false, bad = !(nlo < k && k <= nlo + neq && r <= SB_C);
+                tau = thr_pick(Lb, max(r - 1, 0));
+                const uint32_t nx = r < neq ? thr_pick(Lb, r) : TT_INF;
                 tm = tau & ~fmask;
                 upper = thr_upper(tm, fmask);
 #pragma unroll
@@ -811,7 +831,6 @@ __device__ __forceinline__ void run_rounds_sel(const T2Args &a, const ThrWin &w,
                     }
                 l = layers = ls;
                 cls = cnt;
-                if (nlo != below || neq != nbb) bad = true;   // a byte counter wrapped
                 // layer ls filled / changed the buffer, or (skip mode) changed iff a shell member
                 const bool changed = !skipm || chg;
                 skipm = false;
