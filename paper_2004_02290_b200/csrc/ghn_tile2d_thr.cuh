@@ -360,6 +360,99 @@ __device__ __forceinline__ void thr_rect_slots(const ThrWin &w, int lr, int lc, 
     }
 }
 
+// Lock-step rounds cost the warp's LARGEST candidate count, so the tile's
+// queries are first ordered by their predicted count (the block the first
+// select walks): warps then hold queries of similar work.  The prediction
+// repeats phase A without side effects; a counting sort over the count (0..
+// 255, larger clamped) orders up to TT_SORT queries in shared memory.
+constexpr int TT_SORT = 1024;
+
+template <bool SEL>
+__device__ __forceinline__ int thr_work_key(const T2Args &a, const ThrWin &w, int qq, int t0, int t1, int r_lo,
+                                            int c_lo) {
+    const int32_t qi = a.qorder[qq];
+    double q0, q1;
+    if (a.q_dtype == GHN_F32) {
+        const float2 qf = ((const float2 *)a.Q)[qi];
+        q0 = (double)qf.x;
+        q1 = (double)qf.y;
+    } else {
+        q0 = ((const double *)a.Q)[2 * (int64_t)qi];
+        q1 = ((const double *)a.Q)[2 * (int64_t)qi + 1];
+    }
+    const int64_t cc0 = cell_id(q0, a.w0, a.inv0, a.pow2 & 1u) - a.lo0;
+    const int64_t cc1 = cell_id(q1, a.w1, a.inv1, (a.pow2 >> 1) & 1u) - a.lo1;
+    const int64_t tr0 = (int64_t)t0 * a.T, tc0 = (int64_t)t1 * a.T;
+    if (cc0 < tr0 || cc0 >= tr0 + a.T || cc1 < tc0 || cc1 >= tc0 + a.T || cc0 >= a.ext0 || cc1 >= a.ext1) return 0;
+    const int lr = (int)(cc0 - r_lo), lc = (int)(cc1 - c_lo);
+    const int lmax = max(max((int)cc0, a.ext0 - 1 - (int)cc0), max((int)cc1, a.ext1 - 1 - (int)cc1));
+    int l = 0, cnt = 0;
+    for (;; ++l) {
+        if (l > a.A) return 0;
+        if (l == 0) {
+            int s0, e0;
+            thr_rect_slots(w, lr, lc, 0, 0, 0, s0, e0);
+            cnt = e0 - s0;
+        } else {
+            for (int r = 0; r < 4 * l; ++r) {
+                int ra, rb, ca, cb, s0, e0;
+                thr_shell_rect(l, r, ra, rb, ca, cb);
+                thr_rect_slots(w, lr, lc, ra, ca, cb, s0, e0);
+                cnt += e0 - s0;
+            }
+        }
+        if (cnt >= a.k || l >= lmax) break;
+    }
+    if (SEL && a.mode == GHN_MODE_HEURISTIC && l < lmax && l + 1 <= a.A) {   // run_rounds_sel's skip-ahead
+        const double kc = (double)a.k * (2.0 * l + 1.0) * (2.0 * l + 1.0) / (3.14159265358979 * (double)cnt);
+        const double fc = 0.8 * ((double)l + 0.5);
+        if (kc > fc * fc) {
+            int sc = 0;
+            for (int r = 0; r < 4 * (l + 1); ++r) {
+                int ra, rb, ca, cb, s0, e0;
+                thr_shell_rect(l + 1, r, ra, rb, ca, cb);
+                thr_rect_slots(w, lr, lc, ra, ca, cb, s0, e0);
+                sc += e0 - s0;
+            }
+            if (cnt + sc <= a.sb_capn) cnt += sc;
+        }
+    }
+    return min(cnt, 255);
+}
+
+// ord[0, c1 - c0) = the local indices of queries [c0, c1) sorted by work key.
+template <bool SEL>
+__device__ __forceinline__ void thr_sort_chunk(const T2Args &a, const ThrWin &w, int c0, int c1, int t0, int t1,
+                                               int r_lo, int c_lo, int *hcnt, uint16_t *kr, uint16_t *ord) {
+    for (int i = threadIdx.x; i < 256; i += TT_THREADS) hcnt[i] = 0;
+    __syncthreads();
+    for (int i = threadIdx.x; i < c1 - c0; i += TT_THREADS) {
+        const int key = thr_work_key<SEL>(a, w, c0 + i, t0, t1, r_lo, c_lo);
+        const int rank = atomicAdd(&hcnt[key], 1);
+        kr[2 * i] = (uint16_t)key;
+        kr[2 * i + 1] = (uint16_t)rank;
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {   // exclusive scan of the 256 counters, 8 per lane
+        int v[8], sum = 0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            v[j] = hcnt[threadIdx.x * 8 + j];
+            sum += v[j];
+        }
+        const int incl = warp_inclusive_scan(sum);
+        int run = incl - sum;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            hcnt[threadIdx.x * 8 + j] = run;
+            run += v[j];
+        }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < c1 - c0; i += TT_THREADS) ord[hcnt[kr[2 * i]] + kr[2 * i + 1]] = (uint16_t)i;
+    __syncthreads();
+}
+
 // The tile's queries in rounds of one query per thread.  Per round:
 //  A  (per lane) load the query; l* = the first layer whose block holds k
 //     points (explore.py: every earlier layer leaves the buffer short, so it
@@ -373,14 +466,15 @@ __device__ __forceinline__ void thr_rect_slots(const ThrWin &w, int lr, int lc, 
 //     the list;
 //  D  the vote (predict.py:29-36) and the outputs.
 template <int KM, bool STATS>
-__device__ __forceinline__ void run_rounds_thr(const T2Args &a, const ThrWin &w, int qb, int qe, int t0, int t1,
+__device__ __forceinline__ void run_rounds_thr(const T2Args &a, const ThrWin &w, const uint16_t *ord, int qb, int qe, int t0, int t1,
                                                int r_lo, int c_lo, ThrTotals &tot) {
     const int k = a.k;
     const uint32_t lmask = (uint32_t)a.lmask;
     const int64_t tr0 = (int64_t)t0 * a.T, tc0 = (int64_t)t1 * a.T;
     for (int base = qb; base < qe; base += TT_THREADS) {
-        const int qq = base + (int)threadIdx.x;
-        bool live = qq < qe;   // this lane holds a query still being answered
+        const int qr = base + (int)threadIdx.x;
+        bool live = qr < qe;   // this lane holds a query still being answered
+        const int qq = live ? qb + ord[qr - qb] : 0;
         int32_t qi = 0;
         double q0 = 0.0, q1 = 0.0;
         int64_t cc0 = 0, cc1 = 0;
@@ -622,7 +716,7 @@ __device__ __forceinline__ int sb_bucket32(float2 c, float q0f, float q1f, int b
 }
 
 template <bool STATS>
-__device__ __forceinline__ void run_rounds_sel(const T2Args &a, const ThrWin &w, uint32_t *hist, int qb, int qe,
+__device__ __forceinline__ void run_rounds_sel(const T2Args &a, const ThrWin &w, uint32_t *hist, const uint16_t *ord, int qb, int qe,
                                                int t0, int t1, int r_lo, int c_lo, ThrTotals &tot) {
     const int k = a.k;
     const uint32_t lmask = (uint32_t)a.lmask;
@@ -631,8 +725,9 @@ __device__ __forceinline__ void run_rounds_sel(const T2Args &a, const ThrWin &w,
     const int64_t tr0 = (int64_t)t0 * a.T, tc0 = (int64_t)t1 * a.T;
     uint32_t *myh = hist + threadIdx.x;   // word i of this lane at myh[i * TT_THREADS]
     for (int base = qb; base < qe; base += TT_THREADS) {
-        const int qq = base + (int)threadIdx.x;
-        bool live = qq < qe;
+        const int qr = base + (int)threadIdx.x;
+        bool live = qr < qe;
+        const int qq = live ? qb + ord[qr - qb] : 0;
         int32_t qi = 0;
         double q0 = 0.0, q1 = 0.0;
         float q0f = 0.0f, q1f = 0.0f;
@@ -1052,13 +1147,34 @@ __global__ void __launch_bounds__(TT_THREADS) tile2d_thr_kernel(const T2Args a) 
     __syncthreads();
     const ThrWin w{sxy, sl, loc, R, W, W1};
     ThrTotals tot{0, 0, 0, 0};
-    if (KM == 0) {
-        run_rounds_sel<STATS>(a, w, (uint32_t *)(rstart + a.win + 1), qb, qe, t0, t1, r_lo, c_lo, tot);
-    } else if (KM <= 4) {
+    if (KM > 0 && KM <= 4) {
         for (int qq = qb + (int)threadIdx.x; qq < qe; qq += TT_THREADS)
             process_query_thr<KM, STATS>(a, w, a.qorder[qq], t0, t1, r_lo, c_lo, tot);
+    } else if (KM == 0) {
+        // the sort's counters and (key, rank) pairs live in the histogram area
+        // (free until the rounds start); the order itself stays beside it
+        __shared__ uint16_t s_ord[TT_SORT];
+        uint32_t *hist = (uint32_t *)(rstart + a.win + 1);
+        for (int c0 = qb; c0 < qe; c0 += TT_SORT) {
+            const int c1 = min(c0 + TT_SORT, qe);
+            if (a.sb_sort) {
+                thr_sort_chunk<true>(a, w, c0, c1, t0, t1, r_lo, c_lo, (int *)hist, (uint16_t *)(hist + 256), s_ord);
+            } else {
+                for (int i = threadIdx.x; i < c1 - c0; i += TT_THREADS) s_ord[i] = (uint16_t)i;
+                __syncthreads();
+            }
+            run_rounds_sel<STATS>(a, w, hist, s_ord, c0, c1, t0, t1, r_lo, c_lo, tot);
+            __syncthreads();
+        }
     } else {
-        run_rounds_thr<KM, STATS>(a, w, qb, qe, t0, t1, r_lo, c_lo, tot);
+        __shared__ uint16_t s_ord[TT_SORT];
+        for (int c0 = qb; c0 < qe; c0 += TT_SORT) {
+            const int c1 = min(c0 + TT_SORT, qe);
+            for (int i = threadIdx.x; i < c1 - c0; i += TT_THREADS) s_ord[i] = (uint16_t)i;
+            __syncthreads();
+            run_rounds_thr<KM, STATS>(a, w, s_ord, c0, c1, t0, t1, r_lo, c_lo, tot);
+            __syncthreads();
+        }
     }
     if (STATS && a.totals) {
         const unsigned long long v0 = warp_sum(tot.layers), v1 = warp_sum(tot.cells), v2 = warp_sum(tot.points),
