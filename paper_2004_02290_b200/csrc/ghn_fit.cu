@@ -51,55 +51,70 @@ static DimParams make_dims(int d, const double *widths, const int64_t *lo, const
 __global__ void bounds_init_kernel(int64_t *bounds, unsigned long long *origin_key, int32_t *flags,
                                    int d) {
     int j = threadIdx.x;
-    if (j < d) {
-        bounds[j] = INT64_MAX;
-        bounds[d + j] = INT64_MIN;
+    if (j < d) {   // order keys of the min (origin_key) and max (bounds[d + j]) coordinates
+        bounds[j] = 0;
+        bounds[d + j] = 0;
         origin_key[j] = ~0ull;
     }
     if (j == 0) *flags = 0;
 }
 
-// K1: D > 0 compile-time dims; one point per thread iteration.
+// K1: D > 0 compile-time dims.  floor(x / w) is monotone in x, so the id
+// bounds are the ids of the per-dimension min / max coordinates: the pass
+// only reduces min / max (and the non-finite flag) in the input type, and
+// origin_decode_kernel turns them into ids.  Keys staged as order-preserving
+// uint64 (min in origin_key, max in bounds[d + j]).
 template <typename T, int D>
 __global__ void __launch_bounds__(FIT_THREADS) bounds_kernel(const T *__restrict__ X, int64_t n,
                                                              DimParams p, int64_t *bounds,
                                                              unsigned long long *origin_key,
                                                              int32_t *flags) {
-    int64_t lo[D], hi[D];
-    double mn[D];
+    T mn[D], mx[D];
     bool bad = false;
 #pragma unroll
     for (int j = 0; j < D; ++j) {
-        lo[j] = INT64_MAX;
-        hi[j] = INT64_MIN;
-        mn[j] = INFINITY;
+        mn[j] = (T)INFINITY;
+        mx[j] = (T)-INFINITY;
     }
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-         i += (int64_t)gridDim.x * blockDim.x) {
+    // BU points per thread per iteration, loads issued first
+    constexpr int BU = 4;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    for (; i + (BU - 1) * stride < n; i += BU * stride) {
+        T v[BU][D];
+#pragma unroll
+        for (int u = 0; u < BU; ++u)
+#pragma unroll
+            for (int j = 0; j < D; ++j) v[u][j] = __ldcs(X + (i + u * stride) * D + j);
+#pragma unroll
+        for (int u = 0; u < BU; ++u)
+#pragma unroll
+            for (int j = 0; j < D; ++j) {
+                bad |= !isfinite(v[u][j]);
+                mn[j] = fmin(mn[j], v[u][j]);
+                mx[j] = fmax(mx[j], v[u][j]);
+            }
+    }
+    for (; i < n; i += stride) {
 #pragma unroll
         for (int j = 0; j < D; ++j) {
-            double x = to_double(X[i * D + j]);
-            if (!isfinite(x)) {
-                bad = true;
-                continue;
-            }
-            int64_t c = cell_id(x, p.w[j], p.inv[j], (p.pow2 >> j) & 1u);
-            lo[j] = c < lo[j] ? c : lo[j];
-            hi[j] = c > hi[j] ? c : hi[j];
+            const T x = X[i * D + j];
+            bad |= !isfinite(x);
             mn[j] = fmin(mn[j], x);
+            mx[j] = fmax(mx[j], x);
         }
     }
 #pragma unroll
     for (int j = 0; j < D; ++j) {
-        int64_t l = warp_min(lo[j]);
-        int64_t h = warp_max(hi[j]);
-        double m = mn[j];
+        double m = to_double(mn[j]), M = to_double(mx[j]);
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) m = fmin(m, __shfl_xor_sync(GHN_FULL, m, o));
+        for (int o = 16; o > 0; o >>= 1) {
+            m = fmin(m, __shfl_xor_sync(GHN_FULL, m, o));
+            M = fmax(M, __shfl_xor_sync(GHN_FULL, M, o));
+        }
         if ((threadIdx.x & 31) == 0) {
-            atomicMin((long long *)&bounds[j], (long long)l);
-            atomicMax((long long *)&bounds[D + j], (long long)h);
             if (m != INFINITY) atomicMin(&origin_key[j], dbl_order_key(m));
+            if (M != -INFINITY) atomicMax((unsigned long long *)&bounds[D + j], dbl_order_key(M));
         }
     }
     if (__any_sync(GHN_FULL, bad) && (threadIdx.x & 31) == 0) atomicOr(flags, 1);
@@ -120,17 +135,22 @@ __global__ void __launch_bounds__(FIT_THREADS) bounds_kernel_rt(const T *__restr
                 atomicOr(flags, 1);
                 continue;
             }
-            int64_t c = cell_id(x, p.w[j], p.inv[j], (p.pow2 >> j) & 1u);
-            atomicMin((long long *)&bounds[j], (long long)c);
-            atomicMax((long long *)&bounds[d + j], (long long)c);
             atomicMin(&origin_key[j], dbl_order_key(x));
+            atomicMax((unsigned long long *)&bounds[d + j], dbl_order_key(x));
         }
     }
 }
 
-__global__ void origin_decode_kernel(const unsigned long long *origin_key, double *origin, int d) {
-    int j = threadIdx.x;
-    if (j < d) origin[j] = dbl_from_order_key(origin_key[j]);
+__global__ void origin_decode_kernel(const unsigned long long *origin_key, double *origin, int64_t *bounds,
+                                     DimParams p) {
+    const int j = threadIdx.x, d = p.d;
+    if (j < d) {
+        const double mn = dbl_from_order_key(origin_key[j]);
+        const double mx = dbl_from_order_key((unsigned long long)bounds[d + j]);
+        origin[j] = mn;
+        bounds[j] = cell_id(mn, p.w[j], p.inv[j], (p.pow2 >> j) & 1u);
+        bounds[d + j] = cell_id(mx, p.w[j], p.inv[j], (p.pow2 >> j) & 1u);
+    }
 }
 
 // K2: linear key over the bbox, row-major with dim 0 most significant.
@@ -312,9 +332,17 @@ __device__ __forceinline__ uint32_t point_key(const T *__restrict__ X, int64_t i
 template <typename T>
 __global__ void __launch_bounds__(FIT_THREADS) hist_kernel(const T *__restrict__ X, int64_t n, DimParams p,
                                                            int32_t *__restrict__ counts) {
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-         i += (int64_t)gridDim.x * blockDim.x)
-        atomicAdd(&counts[point_key(X, i, p)], 1);
+    constexpr int BU = 4;   // independent points per iteration (loads and atomics in flight)
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    for (; i + (BU - 1) * stride < n; i += BU * stride) {
+        uint32_t key[BU];
+#pragma unroll
+        for (int u = 0; u < BU; ++u) key[u] = point_key(X, i + u * stride, p);
+#pragma unroll
+        for (int u = 0; u < BU; ++u) atomicAdd(&counts[key[u]], 1);
+    }
+    for (; i < n; i += stride) atomicAdd(&counts[point_key(X, i, p)], 1);
 }
 
 __global__ void max_count_kernel(const int32_t *__restrict__ off, int64_t E, int32_t *out) {
@@ -739,7 +767,7 @@ extern "C" int32_t ghn_fit_bounds(const void *X, int32_t dtype, int64_t n, int32
                      ? bounds_launch<float>((const float *)X, n, d, p, out_bounds, okey, out_flags, s)
                      : bounds_launch<double>((const double *)X, n, d, p, out_bounds, okey, out_flags, s);
     if (rc) return rc;
-    origin_decode_kernel<<<1, 32, 0, s>>>(okey, out_origin, d);
+    origin_decode_kernel<<<1, 32, 0, s>>>(okey, out_origin, out_bounds, p);
     GHN_LAUNCH_CHECK("origin_decode_kernel");
     return GHN_OK;
 }
