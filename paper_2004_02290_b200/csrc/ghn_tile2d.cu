@@ -1110,8 +1110,8 @@ __global__ void window_density_kernel(const int32_t *__restrict__ cell_start, co
 // Largest k answered with the register list; larger k use the bucket select
 // (GHN_TT_LISTMAX overrides, for measurements).
 static int tt_list_kmax() {
-    static const int v = getenv("GHN_TT_LISTMAX") ? atoi(getenv("GHN_TT_LISTMAX")) : TT_LIST_KMAX;
-    return v;
+    const char *e = getenv("GHN_TT_LISTMAX");
+    return e ? atoi(e) : TT_LIST_KMAX;
 }
 
 bool tile2d_plan(const ghn_index_view *ix, int64_t nq, int32_t k, int32_t task, bool want_neighbors,
