@@ -842,7 +842,7 @@ __device__ __forceinline__ void run_rounds_sel(const T2Args &a, const ThrWin &w,
                         bool edge;
                         const int b = f32q ? sb_bucket32(w.xy[p], q0f, q1f, bbase, edge)
                                            : sb_bucket(thr_pack(w.xy[p], q0, q1, 0u, fmask), bbase);
-                        myh[(b >> 2) * TT_THREADS] += 1u << (8 * (b & 3));
+                        atomicAdd(&myh[(b >> 2) * TT_THREADS], 1u << (8 * (b & 3)));   // one RED, private word
                     }
                     p += have ? 1 : 0;
                 }
