@@ -466,13 +466,19 @@ __device__ __forceinline__ void thr_sort_chunk(const T2Args &a, const ThrWin &w,
 //     the list;
 //  D  the vote (predict.py:29-36) and the outputs.
 template <int KM, bool STATS>
-__device__ __forceinline__ void run_rounds_thr(const T2Args &a, const ThrWin &w, const uint16_t *ord, int qb, int qe, int t0, int t1,
+__device__ __forceinline__ void run_rounds_thr(const T2Args &a, const ThrWin &w, const uint16_t *ord, int *s_grp, int qb, int qe, int t0, int t1,
                                                int r_lo, int c_lo, ThrTotals &tot) {
     const int k = a.k;
     const uint32_t lmask = (uint32_t)a.lmask;
     const int64_t tr0 = (int64_t)t0 * a.T, tc0 = (int64_t)t1 * a.T;
-    for (int base = qb; base < qe; base += TT_THREADS) {
-        const int qr = base + (int)threadIdx.x;
+    for (;;) {
+        // the next group of 32 (sorted) queries for this warp: warps that
+        // finish early take more groups instead of waiting at the barrier
+        int g0 = 0;
+        if ((threadIdx.x & 31) == 0) g0 = atomicAdd(s_grp, 32);
+        g0 = __shfl_sync(GHN_FULL, g0, 0);
+        if (g0 >= qe - qb) break;
+        const int qr = qb + g0 + (int)(threadIdx.x & 31);
         bool live = qr < qe;   // this lane holds a query still being answered
         const int qq = live ? qb + ord[qr - qb] : 0;
         int32_t qi = 0;
@@ -716,7 +722,7 @@ __device__ __forceinline__ int sb_bucket32(float2 c, float q0f, float q1f, int b
 }
 
 template <bool STATS>
-__device__ __forceinline__ void run_rounds_sel(const T2Args &a, const ThrWin &w, uint32_t *hist, const uint16_t *ord, int qb, int qe,
+__device__ __forceinline__ void run_rounds_sel(const T2Args &a, const ThrWin &w, uint32_t *hist, const uint16_t *ord, int *s_grp, int qb, int qe,
                                                int t0, int t1, int r_lo, int c_lo, ThrTotals &tot) {
     const int k = a.k;
     const uint32_t lmask = (uint32_t)a.lmask;
@@ -724,8 +730,12 @@ __device__ __forceinline__ void run_rounds_sel(const T2Args &a, const ThrWin &w,
     const bool f32q = a.q_dtype == GHN_F32;   // fp32 queries: fp32 keys prefilter the buckets
     const int64_t tr0 = (int64_t)t0 * a.T, tc0 = (int64_t)t1 * a.T;
     uint32_t *myh = hist + threadIdx.x;   // word i of this lane at myh[i * TT_THREADS]
-    for (int base = qb; base < qe; base += TT_THREADS) {
-        const int qr = base + (int)threadIdx.x;
+    for (;;) {
+        int g0 = 0;   // the next group of 32 (sorted) queries for this warp
+        if ((threadIdx.x & 31) == 0) g0 = atomicAdd(s_grp, 32);
+        g0 = __shfl_sync(GHN_FULL, g0, 0);
+        if (g0 >= qe - qb) break;
+        const int qr = qb + g0 + (int)(threadIdx.x & 31);
         bool live = qr < qe;
         const int qq = live ? qb + ord[qr - qb] : 0;
         int32_t qi = 0;
@@ -1155,24 +1165,28 @@ __global__ void __launch_bounds__(TT_THREADS) tile2d_thr_kernel(const T2Args a) 
         // (free until the rounds start); the order itself stays beside it
         __shared__ uint16_t s_ord[TT_SORT];
         uint32_t *hist = (uint32_t *)(rstart + a.win + 1);
+        __shared__ int s_grp;
         for (int c0 = qb; c0 < qe; c0 += TT_SORT) {
             const int c1 = min(c0 + TT_SORT, qe);
+            if (threadIdx.x == 0) s_grp = 0;
             if (a.sb_sort) {
                 thr_sort_chunk<true>(a, w, c0, c1, t0, t1, r_lo, c_lo, (int *)hist, (uint16_t *)(hist + 256), s_ord);
             } else {
                 for (int i = threadIdx.x; i < c1 - c0; i += TT_THREADS) s_ord[i] = (uint16_t)i;
                 __syncthreads();
             }
-            run_rounds_sel<STATS>(a, w, hist, s_ord, c0, c1, t0, t1, r_lo, c_lo, tot);
+            run_rounds_sel<STATS>(a, w, hist, s_ord, &s_grp, c0, c1, t0, t1, r_lo, c_lo, tot);
             __syncthreads();
         }
     } else {
         __shared__ uint16_t s_ord[TT_SORT];
+        __shared__ int s_grp;
         for (int c0 = qb; c0 < qe; c0 += TT_SORT) {
             const int c1 = min(c0 + TT_SORT, qe);
+            if (threadIdx.x == 0) s_grp = 0;
             for (int i = threadIdx.x; i < c1 - c0; i += TT_THREADS) s_ord[i] = (uint16_t)i;
             __syncthreads();
-            run_rounds_thr<KM, STATS>(a, w, s_ord, c0, c1, t0, t1, r_lo, c_lo, tot);
+            run_rounds_thr<KM, STATS>(a, w, s_ord, &s_grp, c0, c1, t0, t1, r_lo, c_lo, tot);
             __syncthreads();
         }
     }
