@@ -737,7 +737,9 @@ __device__ __forceinline__ void run_rounds_sel(const T2Args &a, const ThrWin &w,
         if (g0 >= qe - qb) break;
         const int qr = qb + g0 + (int)(threadIdx.x & 31);
         bool live = qr < qe;
-        const int qq = live ? qb + ord[qr - qb] : 0;
+        // heaviest groups first (ord is ascending in predicted work): the
+        // CTA's tail is then a light group
+        const int qq = live ? qb + ord[qe - 1 - qr] : 0;
         int32_t qi = 0;
         double q0 = 0.0, q1 = 0.0;
         float q0f = 0.0f, q1f = 0.0f;
