@@ -328,6 +328,11 @@ struct RectBound {
         fh1 = (double)(a.lo1 + cc1 + 1) * a.w1 - q1;
         margin = 1e-9 * fmax(a.w0, a.w1) + 1e-12 * (fabs(q0) + fabs(q1));
     }
+    // no point of shell(l) can precede `upper` (the face of block(l - 1))
+    __device__ __forceinline__ bool shell_beyond(const T2Args &a, int l, double upper) const {
+        const double d = fmin(fmin(fl0, fh0) + (double)(l - 1) * a.w0, fmin(fl1, fh1) + (double)(l - 1) * a.w1) - margin;
+        return d > 0.0 && d * d * (1.0 - 1e-9) > upper;
+    }
     __device__ __forceinline__ bool beyond(const T2Args &a, int ra, int rb, int ca, int cb, double upper) const {
         double dx = ra > 0 ? fh0 + (double)(ra - 1) * a.w0 : (rb < 0 ? fl0 + (double)(-rb - 1) * a.w0 : 0.0);
         double dy = ca > 0 ? fh1 + (double)(ca - 1) * a.w1 : (cb < 0 ? fl1 + (double)(-cb - 1) * a.w1 : 0.0);
@@ -588,7 +593,9 @@ __device__ __forceinline__ void run_rounds_thr(const T2Args &a, const ThrWin &w,
             {
                 int r = 0, p = 0, e = 0;
                 const int nr = 4 * l;
-                bool act = more;
+                // the whole shell first (one test); per range only if it may matter
+                bool act = more && !rb0.shell_beyond(a, l, upper);
+                if (STATS && more && !act) sc = thr_shell_count(w, lr, lc, l);
                 for (;;) {
                     while (act && p >= e) {
                         if (r >= nr) {
@@ -967,7 +974,9 @@ __device__ __forceinline__ void run_rounds_sel(const T2Args &a, const ThrWin &w,
                 {
                     int rr = 0, p = 0, e = 0;
                     const int nr = 4 * l;
-                    bool act = more;
+                    // the whole shell first (one test); per range only if it may matter
+                    bool act = more && !rb0.shell_beyond(a, l, upper);
+                    if (more && !act) sc = thr_shell_count(w, lr, lc, l);
                     for (;;) {
                         while (act && p >= e) {
                             if (rr >= nr) {
