@@ -857,12 +857,13 @@ __device__ __forceinline__ void run_rounds_sel(const T2Args &a, const ThrWin &w,
                         ++ra;
                         thr_rect_slots(w, lr, lc, ra, -ls, ls, p, e);
                     }
-                    if (have) {   // approximate buckets are fine here: pass 2 recounts exactly
-                        bool edge;
-                        const int b = f32q ? sb_bucket32(w.xy[p], q0f, q1f, bbase, edge)
-                                           : sb_bucket(thr_pack(w.xy[p], q0, q1, 0u, fmask), bbase);
-                        atomicAdd(&myh[(b >> 2) * TT_THREADS], 1u << (8 * (b & 3)));   // one RED, private word
-                    }
+                    // approximate buckets are fine here: pass 2 recounts exactly.
+                    // Branch-free: an idle lane adds 0 to its own word.
+                    const int pp = have ? p : 0;
+                    bool edge;
+                    const int b = f32q ? sb_bucket32(w.xy[pp], q0f, q1f, bbase, edge)
+                                       : sb_bucket(thr_pack(w.xy[pp], q0, q1, 0u, fmask), bbase);
+                    atomicAdd(&myh[(b >> 2) * TT_THREADS], have ? 1u << (8 * (b & 3)) : 0u);   // one RED, private word
                     p += have ? 1 : 0;
                 }
             }
@@ -915,11 +916,10 @@ __device__ __forceinline__ void run_rounds_sel(const T2Args &a, const ThrWin &w,
                     const uint32_t lab = (uint32_t)w.sl[pp] | (insh ? lmask + 1u : 0u);
                     const uint32_t pk = thr_pack(w.xy[pp], q0, q1, lab, fmask);
                     const int b = sb_bucket(pk, bbase);
-                    if (have && b < bb) {
-                        cn += 1ull << (8 * (lab & lmask));
-                        chg |= insh;
-                        ++nlo;
-                    }
+                    const bool low = have && b < bb;   // branch-free vote below the boundary bucket
+                    cn += low ? 1ull << (8 * (lab & lmask)) : 0ull;
+                    chg |= low && insh;
+                    nlo += low ? 1 : 0;
                     const bool inb = have && b == bb;
                     neq += inb ? 1 : 0;
                     if (__any_sync(GHN_FULL, inb)) thr_bubble(Lb, inb ? pk : TT_INF);
