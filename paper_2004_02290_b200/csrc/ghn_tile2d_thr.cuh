@@ -29,6 +29,8 @@
 // shared helpers (T2Args, ShellBound, push_fallback).
 #pragma once
 
+#include "ghn_nets.cuh"
+
 namespace ghn {
 namespace {
 
@@ -544,17 +546,26 @@ __device__ __forceinline__ void run_rounds_thr(const T2Args &a, const ThrWin &w,
             const int steps = __reduce_max_sync(GHN_FULL, n);
             int ra = -l, p = 0, e = 0;
             if (live) thr_rect_slots(w, lr, lc, ra, -l, l, p, e);
-            for (int it = 0; it < steps; ++it) {
-                const bool have = it < n;
-                while (have && p >= e) {
-                    ++ra;
-                    thr_rect_slots(w, lr, lc, ra, -l, l, p, e);
+            // batches of 8 candidates per lane: sorted by a 19-comparator
+            // network, then merged into the list (NetMerge8: 41 comparators
+            // at k = 16) -- 15 min/max pairs per candidate instead of the
+            // bubble's k + 1
+            for (int it = 0; it < steps; it += 8) {
+                uint32_t bt[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const bool have = it + u < n;
+                    while (have && p >= e) {
+                        ++ra;
+                        thr_rect_slots(w, lr, lc, ra, -l, l, p, e);
+                    }
+                    const int pp = have ? p : 0;
+                    const uint32_t pk = thr_pack(w.xy[pp], q0, q1, (uint32_t)w.sl[pp], lmask);
+                    bt[u] = have ? pk : TT_INF;
+                    p += have ? 1 : 0;
                 }
-                const int pp = have ? p : 0;
-                uint32_t pk = thr_pack(w.xy[pp], q0, q1, (uint32_t)w.sl[pp], lmask);
-                pk = have ? pk : TT_INF;
-                thr_bubble(L, pk);
-                p += have ? 1 : 0;
+                net_sort8(bt);
+                NetMerge8<KM + 1>::run(L, bt);
             }
         }
         int layers = l;
@@ -1168,10 +1179,10 @@ __global__ void __launch_bounds__(TT_THREADS) tile2d_thr_kernel(const T2Args a) 
     __syncthreads();
     const ThrWin w{sxy, sl, loc, R, W, W1};
     ThrTotals tot{0, 0, 0, 0};
-    if (KM > 0 && KM <= 4) {
+    if constexpr (KM > 0 && KM <= 4) {
         for (int qq = qb + (int)threadIdx.x; qq < qe; qq += TT_THREADS)
             process_query_thr<KM, STATS>(a, w, a.qorder[qq], t0, t1, r_lo, c_lo, tot);
-    } else if (KM == 0) {
+    } else if constexpr (KM == 0) {
         // the sort's counters and (key, rank) pairs live in the histogram area
         // (free until the rounds start); the order itself stays beside it
         __shared__ uint16_t s_ord[TT_SORT];
