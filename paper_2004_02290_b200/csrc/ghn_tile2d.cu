@@ -79,6 +79,7 @@ struct T2Args {
     int32_t small_labels;
     int32_t lmask;   // label-code mask of the thread kernel (2^LB - 1)
     int32_t sb_capn, sb_redo, sb_wmax, sb_sort;   // bucket-select lock-step knobs (see ghn_tile2d_thr.cuh)
+    double tt_skipf;   // k = 3, 4 rounds: skip-ahead threshold (fraction of the block half-width)
 };
 
 struct Win {
@@ -1264,6 +1265,7 @@ int32_t tile2d_run(const ghn_index_view *ix, const Tile2dPlan *plan, const void 
     a.sb_redo = getenv("GHN_SB_REDO") ? atoi(getenv("GHN_SB_REDO")) : 2;
     a.sb_wmax = getenv("GHN_SB_WMAX") ? atoi(getenv("GHN_SB_WMAX")) : 0;
     a.sb_sort = getenv("GHN_SB_SORT") ? atoi(getenv("GHN_SB_SORT")) : 1;
+    a.tt_skipf = getenv("GHN_TT_SKIPF") ? atof(getenv("GHN_TT_SKIPF")) : 0.4;
     const bool stats = out->stats != nullptr || out->totals != nullptr;
     // warp kernel: extraction select for small k (EXT), histogram select otherwise
     int ki = plan->G == 8 ? 1 : (plan->G == 16 ? 2 : (k >= 2 && k <= T2_EXT_MAXK ? 3 : 0));

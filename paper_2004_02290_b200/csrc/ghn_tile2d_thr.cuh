@@ -131,7 +131,8 @@ struct ThrTotals {
 // Vote over the list's first k entries (predict.py:29-36).  False = the
 // tie-break needs exact keys (generic kernel).
 template <int KM>
-__device__ __forceinline__ bool thr_vote(const uint32_t (&L)[KM + 1], int k, uint32_t lmask, int &wl, int &top) {
+__device__ __forceinline__ bool thr_vote(const uint32_t (&L)[KM + 1], int k, uint32_t lmask, int &wl, int &top,
+                                         uint32_t dmask = 0u) {
     uint64_t cn = 0;   // 8-bit counter per label code
 #pragma unroll
     for (int j = 0; j < KM; ++j)
@@ -162,7 +163,7 @@ __device__ __forceinline__ bool thr_vote(const uint32_t (&L)[KM + 1], int k, uin
             if (tied && w1 == TT_INF) w1 = L[j];
             else if (tied && w2 == TT_INF && lab != (w1 & lmask)) w2 = L[j];
         }
-        const int lb = __popc(lmask);
+        const int lb = __popc(dmask ? dmask : lmask);   // bits below the d-part
         if ((w2 >> lb) - (w1 >> lb) < 2u) return false;
         wl = (int)(w1 & lmask);
     }
@@ -477,6 +478,9 @@ __device__ __forceinline__ void run_rounds_thr(const T2Args &a, const ThrWin &w,
                                                int r_lo, int c_lo, ThrTotals &tot) {
     const int k = a.k;
     const uint32_t lmask = (uint32_t)a.lmask;
+    constexpr bool SKIP_AHEAD = KM == 4;
+    // label bits + the shell flag above them (skip-ahead only)
+    const uint32_t fmask = SKIP_AHEAD ? 2u * lmask + 1u : lmask;
     const int64_t tr0 = (int64_t)t0 * a.T, tc0 = (int64_t)t1 * a.T;
     for (;;) {
         // the next group of 32 (sorted) queries for this warp: warps that
@@ -537,6 +541,28 @@ __device__ __forceinline__ void run_rounds_thr(const T2Args &a, const ThrWin &w,
                 ++l;
             }
         }
+        // Skip-ahead (heuristic mode): when block(l*) is barely full the next
+        // shell will most likely change the top-k, so select over block(l*+1)
+        // at once; changed(l*+1) is read off a flag on shell(l*+1)'s points.
+        // Compiled for the 4-slot list only (k = 3, 4): at k = 16 the next
+        // shell rarely changes and the extra registers cost a CTA per SM.
+        bool skipm = false;
+        if (SKIP_AHEAD && live && a.mode == GHN_MODE_HEURISTIC && l < lmax && l + 1 <= a.A) {
+            const double kc = (double)k * (2.0 * l + 1.0) * (2.0 * l + 1.0) / (3.14159265358979 * (double)cnt);
+            const double fc = a.tt_skipf * ((double)l + 0.5);
+            if (kc > fc * fc) {
+                int sc = 0;
+                for (int r = 0; r < 4 * (l + 1); ++r) {
+                    int ra, rb, ca, cb, s0, e0;
+                    thr_shell_rect(l + 1, r, ra, rb, ca, cb);
+                    thr_rect_slots(w, lr, lc, ra, ca, cb, s0, e0);
+                    sc += e0 - s0;
+                }
+                skipm = true;
+                ++l;
+                cnt += sc;
+            }
+        }
         // ---- B: block(l) row by row, lock-step
         uint32_t L[KM + 1];
 #pragma unroll
@@ -544,8 +570,11 @@ __device__ __forceinline__ void run_rounds_thr(const T2Args &a, const ThrWin &w,
         {
             const int n = live ? cnt : 0;
             const int steps = __reduce_max_sync(GHN_FULL, n);
-            int ra = -l, p = 0, e = 0;
-            if (live) thr_rect_slots(w, lr, lc, ra, -l, l, p, e);
+            int ra = -l, p = 0, e = 0, pi0 = 0, pi1 = 0;
+            if (live) {
+                thr_rect_slots(w, lr, lc, ra, -l, l, p, e);
+                if (SKIP_AHEAD) thr_rect_slots(w, lr, lc, ra, -(l - 1), l - 1, pi0, pi1);
+            }
             // batches of 8 candidates per lane: sorted by a 19-comparator
             // network, then merged into the list (NetMerge8: 41 comparators
             // at k = 16) -- 15 min/max pairs per candidate instead of the
@@ -558,24 +587,46 @@ __device__ __forceinline__ void run_rounds_thr(const T2Args &a, const ThrWin &w,
                     while (have && p >= e) {
                         ++ra;
                         thr_rect_slots(w, lr, lc, ra, -l, l, p, e);
+                        if (SKIP_AHEAD) thr_rect_slots(w, lr, lc, ra, -(l - 1), l - 1, pi0, pi1);
                     }
                     const int pp = have ? p : 0;
-                    const uint32_t pk = thr_pack(w.xy[pp], q0, q1, (uint32_t)w.sl[pp], lmask);
+                    const bool insh = SKIP_AHEAD && skipm && (ra == -l || ra == l || pp < pi0 || pp >= pi1);
+                    const uint32_t pk =
+                        thr_pack(w.xy[pp], q0, q1, (uint32_t)w.sl[pp] | (insh ? lmask + 1u : 0u), fmask);
                     bt[u] = have ? pk : TT_INF;
                     p += have ? 1 : 0;
                 }
-                net_sort8(bt);
-                NetMerge8<KM + 1>::run(L, bt);
+                if constexpr (KM <= 2) {   // a list of 2-3: the bubble is cheaper than sort + merge
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) thr_bubble(L, bt[u]);
+                } else {
+                    net_sort8(bt);
+                    NetMerge8<KM + 1>::run(L, bt);
+                }
             }
         }
         int layers = l;
         int64_t points = cnt;
+        if (SKIP_AHEAD && live && skipm) {
+            // changed(l*+1) <=> a member of T_{l*+1} carries the shell flag;
+            // membership needs a clean k-th boundary
+            const uint32_t tau = thr_pick(L, k - 1), nx = thr_pick(L, k);
+            bool chg = false;
+#pragma unroll
+            for (int j = 0; j < KM; ++j) chg |= j < k && (L[j] & (lmask + 1u)) != 0u;
+            if (nx != TT_INF && (nx & ~fmask) == (tau & ~fmask)) {
+                push_fallback(a, qi);
+                live = false;
+            } else if (!chg) {
+                lmax = l;   // heuristic stop at l*+1
+            }
+        }
         // stop rules after layer l* (it filled the buffer: changed)
         if (live && cnt >= k && a.mode == GHN_MODE_GUARANTEED) {
             const double b = __dmul_rn((double)l, a.min_w);
             const double b2 = __dmul_rn(b, b);
-            const uint32_t tk = thr_pick(L, k - 1) & ~lmask;
-            if (b2 >= thr_upper(tk, lmask)) {
+            const uint32_t tk = thr_pick(L, k - 1) & ~fmask;
+            if (b2 >= thr_upper(tk, fmask)) {
                 lmax = l;   // stop
             } else if (b2 > thr_lower(tk)) {
                 push_fallback(a, qi);
@@ -595,8 +646,8 @@ __device__ __forceinline__ void run_rounds_thr(const T2Args &a, const ThrWin &w,
                     push_fallback(a, qi);
                     more = false;
                 }
-                tm = thr_pick(L, k - 1) & ~lmask;
-                upper = thr_upper(tm, lmask);
+                tm = thr_pick(L, k - 1) & ~fmask;
+                upper = thr_upper(tm, fmask);
             }
             // compare-only scan of the shell's ranges that may hold a point preceding the k-th
             bool lt = false, eq = false;
@@ -622,9 +673,9 @@ __device__ __forceinline__ void run_rounds_thr(const T2Args &a, const ThrWin &w,
                     }
                     if (!__any_sync(GHN_FULL, act)) break;
                     const int pp = act ? p : 0;
-                    const uint32_t pk = thr_pack(w.xy[pp], q0, q1, (uint32_t)w.sl[pp], lmask);
+                    const uint32_t pk = thr_pack(w.xy[pp], q0, q1, (uint32_t)w.sl[pp], fmask);
                     lt |= act && pk < tm;
-                    eq |= act && (uint32_t)(pk - tm) <= lmask;
+                    eq |= act && (uint32_t)(pk - tm) <= fmask;
                     p += act ? 1 : 0;
                 }
             }
@@ -651,7 +702,7 @@ __device__ __forceinline__ void run_rounds_thr(const T2Args &a, const ThrWin &w,
                     }
                     if (!__any_sync(GHN_FULL, redo)) break;
                     const int pp = redo ? p : 0;
-                    uint32_t pk = thr_pack(w.xy[pp], q0, q1, (uint32_t)w.sl[pp], lmask);
+                    uint32_t pk = thr_pack(w.xy[pp], q0, q1, (uint32_t)w.sl[pp], fmask);
                     pk = redo ? pk : TT_INF;
                     thr_bubble(L, pk);
                     p += redo ? 1 : 0;
@@ -664,8 +715,8 @@ __device__ __forceinline__ void run_rounds_thr(const T2Args &a, const ThrWin &w,
                 if (a.mode == GHN_MODE_GUARANTEED) {
                     const double b = __dmul_rn((double)l, a.min_w);
                     const double b2 = __dmul_rn(b, b);
-                    const uint32_t tk = thr_pick(L, k - 1) & ~lmask;
-                    if (b2 >= thr_upper(tk, lmask)) {
+                    const uint32_t tk = thr_pick(L, k - 1) & ~fmask;
+                    if (b2 >= thr_upper(tk, fmask)) {
                         stop = true;
                     } else if (b2 > thr_lower(tk)) {
                         push_fallback(a, qi);
@@ -682,7 +733,7 @@ __device__ __forceinline__ void run_rounds_thr(const T2Args &a, const ThrWin &w,
         if (fin) {
             const uint32_t tau = thr_pick(L, k - 1), nx = thr_pick(L, k);
             int wl, top;
-            if ((nx != TT_INF && (nx & ~lmask) == (tau & ~lmask)) || !thr_vote<KM>(L, k, lmask, wl, top)) {
+            if ((nx != TT_INF && (nx & ~fmask) == (tau & ~fmask)) || !thr_vote<KM>(L, k, lmask, wl, top, fmask)) {
                 push_fallback(a, qi);
             } else {
                 if (a.out_label) a.out_label[qi] = wl;
@@ -1179,7 +1230,7 @@ __global__ void __launch_bounds__(TT_THREADS) tile2d_thr_kernel(const T2Args a) 
     __syncthreads();
     const ThrWin w{sxy, sl, loc, R, W, W1};
     ThrTotals tot{0, 0, 0, 0};
-    if constexpr (KM > 0 && KM <= 4) {
+    if constexpr (KM > 0 && KM <= 2) {   // k <= 2: each lane on its own loop
         for (int qq = qb + (int)threadIdx.x; qq < qe; qq += TT_THREADS)
             process_query_thr<KM, STATS>(a, w, a.qorder[qq], t0, t1, r_lo, c_lo, tot);
     } else if constexpr (KM == 0) {
