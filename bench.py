@@ -387,43 +387,67 @@ def run_ours(args):
         out_key = "label" if w.task == "classify" else "value"
         out_dt = torch.int32 if w.task == "classify" else torch.float64
         outs_h = [torch.empty(nq, dtype=out_dt).pin_memory() for _ in ks]
-        copy_stream = torch.cuda.Stream(device=dev)
+        # Streaming pipeline over the K timed steps: step i+1's queries are
+        # copied H2D (pinned, own stream, double-buffered) while step i
+        # predicts; each k's labels go back D2H on another stream while the
+        # next k computes.  Every step's H2D and D2H are inside the timed
+        # region (the first H2D and the last D2H are not overlapped).
+        in_stream = torch.cuda.Stream(device=dev)
+        out_stream = torch.cuda.Stream(device=dev)
+        bufs = [torch.empty_like(Q_d) for _ in range(2)]
 
-        def e2e_step():
-            Qd = Q_h.to(dev, non_blocking=True)
-            for j, k in enumerate(ks):
-                r = predict_batch(index, Qd, k, task=w.task, confidence=False)
-                res = r[out_key]
-                ev = torch.cuda.Event()
+        def e2e_run(nsteps):
+            h2d = [torch.cuda.Event() for _ in range(2)]
+            free = [torch.cuda.Event() for _ in range(2)]
+            for ev in free:
                 ev.record(stream)
-                copy_stream.wait_event(ev)
-                with torch.cuda.stream(copy_stream):
-                    outs_h[j].copy_(res, non_blocking=True)
-                res.record_stream(copy_stream)
+
+            def issue_h2d(i):
+                b = i % 2
+                in_stream.wait_event(free[b])   # the buffer's previous step has finished reading it
+                with torch.cuda.stream(in_stream):
+                    bufs[b].copy_(Q_h, non_blocking=True)
+                h2d[b].record(in_stream)
+
+            issue_h2d(0)
+            for i in range(nsteps):
+                b = i % 2
+                if i + 1 < nsteps:
+                    issue_h2d(i + 1)
+                stream.wait_event(h2d[b])
+                for j, k in enumerate(ks):
+                    r = predict_batch(index, bufs[b], k, task=w.task, confidence=False)
+                    res = r[out_key]
+                    ev = torch.cuda.Event()
+                    ev.record(stream)
+                    out_stream.wait_event(ev)
+                    with torch.cuda.stream(out_stream):
+                        outs_h[j].copy_(res, non_blocking=True)
+                    res.record_stream(out_stream)
+                free[b].record(stream)
             done = torch.cuda.Event()
-            done.record(copy_stream)
+            done.record(out_stream)
             stream.wait_event(done)
 
-        e2e_step()
+        e2e_run(2)
         torch.cuda.synchronize()
-        e2e_ms = 0.0
-        for _ in range(args.steps):
-            flush.zero_()
-            barrier(world)
-            torch.cuda.synchronize()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            e2e_step()
-            e1.record(stream)
-            torch.cuda.synchronize()
-            e2e_ms += e0.elapsed_time(e1)
-        e2e_ms = max_over_ranks(e2e_ms / args.steps, world)
+        barrier(world)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        e2e_run(args.steps)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        barrier(world)
+        e2e_ms = max_over_ranks(e0.elapsed_time(e1) / args.steps, world)
         e2e = {"value": world * queries_per_step / (e2e_ms / 1e3), "unit": "queries/s",
                "h2d_bytes_per_step": int(Q_h.numel() * Q_h.element_size()),
                "d2h_bytes_per_step": sum(int(o.numel() * o.element_size()) for o in outs_h),
                "ms_per_step": e2e_ms,
-               "pipeline": "one pinned H2D of the step's queries; per-k D2H of the predictions on a "
-                           "copy stream overlapping the next k's predict"}
+               "pipeline": "K steps back to back: each step's queries H2D from pinned memory on a copy "
+                           "stream, double-buffered so step i+1's copy overlaps step i's predicts; each "
+                           "k's labels D2H on a second copy stream overlapping the next k; the first "
+                           "H2D and the last D2H are exposed; no L2 flush (training data 800 MB > L2)"}
 
     # ---- CPU legs (rank 0, N=1 only)
     cpu_baseline = None
