@@ -81,3 +81,32 @@ def test_label_codes_2_and_8(ghn, n_labels, k):
     index = ghn.build_arrays(X, y, cells_per_axis=500)
     ref = oracle.COracle(X, np.full(2, 1.0 / 500))
     _check(ghn, index, ref, y, Q, k, "heuristic")
+
+
+@pytest.mark.parametrize("k", [1, 4, 16, 64, 200])
+@pytest.mark.parametrize("n_labels", [1, 8])
+def test_sparse_small_sets(ghn, k, n_labels):
+    """Few points over many cells (most queries need far layers or fall back),
+    a single class, k close to n: still exact."""
+    rng = np.random.default_rng(31 + k + n_labels)
+    X = rng.random((600, 2), dtype=np.float32)
+    y = rng.integers(0, n_labels, X.shape[0]).astype(np.int32)
+    Q = rng.random((6000, 2), dtype=np.float32)
+    index = ghn.build_arrays(X, y, cells_per_axis=64)
+    ref = oracle.COracle(X, np.full(2, 1.0 / 64))
+    _check(ghn, index, ref, y, Q, k, "heuristic")
+    _check(ghn, index, ref, y, Q[:2000], k, "guaranteed")
+
+
+def test_heavy_duplicates_small_k(ghn):
+    """Exact duplicate points (equal keys) inside the lists and at the k-th
+    boundary for the register-list and skip-ahead paths."""
+    rng = np.random.default_rng(77)
+    X = rng.random((300_000, 2), dtype=np.float32)
+    X[::5] = X[1::5]                       # every point has a twin
+    y = rng.integers(0, 4, X.shape[0]).astype(np.int32)
+    Q = np.concatenate([rng.random((20_000, 2), dtype=np.float32), X[:5000]])
+    index = ghn.build_arrays(X, y, cells_per_axis=220)
+    ref = oracle.COracle(X, np.full(2, 1.0 / 220))
+    for k in (1, 2, 3, 4, 8, 16, 33):
+        _check(ghn, index, ref, y, Q, k, "heuristic")
