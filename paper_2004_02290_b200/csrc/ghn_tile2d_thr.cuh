@@ -1,32 +1,41 @@
 // ghn_tile2d_thr.cuh -- thread-per-query variant of the tiled 2-D classify
-// (explore.py:66-137 + predict.py:20-36), for k <= 32 and <= 8 label codes.
+// (explore.py:66-137 + predict.py:20-36), for k <= 255 and <= 8 label codes.
 //
-// Each thread answers one query over the staged window with a register-
-// resident list of the k+1 smallest PACKED keys of the candidates seen:
+// Each thread answers one query over the staged window, keeping PACKED keys:
 //
 //   packed = bits[62..31] of the fp64 key (exponent + 21 mantissa bits; the
-//            sign is 0), low LB bits replaced by the label code.
+//            sign is 0), low bits replaced by the label code (and, where a
+//            path skips ahead, a shell flag above it).
 //
 // Truncating the IEEE pattern of a non-negative double is monotone, so the
-// "d-part" (packed >> LB) of a key is a non-decreasing function of the exact
-// key: sorting candidates by exact (key, index) also sorts them by d-part.
-// Hence, with tau = the k-th smallest packed value and D(.) the d-part:
+// "d-part" (packed without its low bits) is a non-decreasing function of the
+// exact key: sorting candidates by exact (key, index) also sorts them by
+// d-part.  Hence, with tau = the k-th smallest packed value and D(.) the
+// d-part:
 //   * the k smallest d-parts are exactly the d-parts of the exact top-k, and
 //     D(tau) = D(exact k-th key);
 //   * a shell point precedes the exact k-th iff D(p) < D(tau) when
 //     D(p) != D(tau) (explore.py:117 `changed`);
-//   * when D(list[k]) > D(tau) the top-k SET is {candidates with D <= D(tau)}
-//     and the list holds exactly their labels, so the vote reads the list.
+//   * when the (k+1)-th d-part exceeds D(tau) the top-k SET is {candidates
+//     with D <= D(tau)} and their labels are known, so the vote needs no
+//     point index.
 // Every case the d-parts cannot decide (equal d-parts across the k-th
 // boundary, a guaranteed-stop bound inside the k-th key's d-part interval,
 // a vote tie-break between members less than two d-units apart) sends the
 // query to the generic exact kernel -- rare (keys must agree to ~2^-18
 // relative) and always correct.
 //
-// The list update is a branch-free min/max bubble (2 integer ops per slot),
-// so the 32 queries of a warp advance in lock-step over their candidates;
-// only their candidate counts differ.  Included by ghn_tile2d.cu after the
-// shared helpers (T2Args, ShellBound, push_fallback).
+// Three shapes, chosen per k (tile2d_thr_kernel):
+//   k <= 2      each lane walks its own layers; branch-free min/max bubble
+//               into a list of k+1 (process_query_thr);
+//   3 <= k <= 32  warp lock-step rounds: block(l*) in batches of 8 sorted by
+//               a network and merged into the list (ghn_nets.cuh), later
+//               shells compare-only; k = 3-4 skip ahead to block(1)
+//               (run_rounds_thr);
+//   k > 32      bucket select: a histogram pass and a vote + boundary-list
+//               pass (run_rounds_sel).
+// Included by ghn_tile2d.cu after the shared helpers (T2Args, ShellBound,
+// push_fallback).
 #pragma once
 
 #include "ghn_nets.cuh"
