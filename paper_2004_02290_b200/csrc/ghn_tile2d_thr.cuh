@@ -180,9 +180,10 @@ __device__ __forceinline__ bool thr_vote(const uint32_t (&L)[KM + 1], int k, uin
 }
 
 // One query on one thread, each lane on its own (no lock-step): the best
-// shape for k <= 4, where the bubble is short and lanes that need more
-// layers should not hold the warp (measured: k = 1 / 4 faster than the
-// lock-step rounds below, k = 16 slower).
+// shape for k <= 2, where the bubble is short and lanes that need more
+// layers should not hold the warp (measured at k = 1: 2.4 ms against 3.6
+// for the lock-step rounds below and 2.8 with their skip-ahead; at k = 4 the
+// skip-ahead rounds win, 2.8 against 3.4).
 template <int KM, bool STATS>
 __device__ __forceinline__ void process_query_thr(const T2Args &a, const ThrWin &w, int32_t qi, int t0, int t1,
                                                   int r_lo, int c_lo, ThrTotals &tot) {
