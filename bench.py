@@ -486,6 +486,7 @@ def run_ours(args):
             "per_k": per_k,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "peak_kind": peak_kind,
+                         "frac_vs_8000_GBps": achieved / 8000.0,   # the north_star's nominal B200 figure
                          "traffic": ncu_traffic(cfg, ks),
                          "kernel": "ghn_query: tile2d_thr_kernel, thread per query (+ binning, + query_kernel fallbacks); "
                                    "time = whole predict call, not the kernel alone",
