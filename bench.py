@@ -83,6 +83,19 @@ def issue_roofline():
         return None
 
 
+def ncu_kernel_stats(cfg, ks):
+    """L2 hit rate and branch uniformity of the predict kernel per k (committed ncu summary)."""
+    p = os.path.join(REPO, "profiles", "ncu_summary.json")
+    try:
+        with open(p) as fh:
+            m = json.load(fh)[f"cfg{cfg}"]
+        return {"l2_hit_pct": {str(k): m["l2_hit_pct"][str(k)] for k in ks},
+                "branch_uniformity_pct": {str(k): m["branch_uniformity_pct"][str(k)] for k in ks},
+                "source": "profiles/ncu_summary.json"}
+    except Exception:
+        return None
+
+
 def ncu_traffic(cfg, ks):
     """Per-launch DRAM bytes of the predict kernel from the committed ncu summary."""
     p = os.path.join(REPO, "profiles", "ncu_summary.json")
@@ -491,7 +504,8 @@ def run_ours(args):
                          "kernel": "ghn_query: tile2d_thr_kernel, thread per query (+ binning, + query_kernel fallbacks); "
                                    "time = whole predict call, not the kernel alone",
                          "algorithmic_bytes_per_step": sum(algo_bytes.values()),
-                         "issue_roofline": issue_roofline()},
+                         "issue_roofline": issue_roofline(),
+                         "kernel_stats": ncu_kernel_stats(cfg, ks)},
             "e2e": e2e,
             "gpu_launches": launches // args.steps,
             "gpu_launches_total": launches,
