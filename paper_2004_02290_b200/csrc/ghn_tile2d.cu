@@ -1051,7 +1051,7 @@ namespace {
 __global__ void tile_key_kernel(const void *Q, int32_t q_dtype, int64_t nq, double w0, double w1,
                                 double inv0, double inv1, uint32_t pow2, int64_t lo0, int64_t lo1,
                                 int32_t ext0, int32_t ext1, int32_t T, int32_t nt1, int32_t *keys,
-                                int32_t *counts) {
+                                int32_t *ranks, int32_t *counts) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nq;
          i += (int64_t)gridDim.x * blockDim.x) {
         double q0, q1;
@@ -1068,17 +1068,16 @@ __global__ void tile_key_kernel(const void *Q, int32_t q_dtype, int64_t nq, doub
         c1 = c1 < 0 ? 0 : (c1 >= ext1 ? ext1 - 1 : c1);
         const int32_t key = (int32_t)(c0 / T) * nt1 + (int32_t)(c1 / T);
         keys[i] = key;
-        atomicAdd(&counts[key], 1);
+        ranks[i] = atomicAdd(&counts[key], 1);   // the query's slot inside its tile
     }
 }
 
-__global__ void tile_scatter_kernel(const int32_t *keys, int64_t nq, const int32_t *tile_start,
-                                    int32_t *cursor, int32_t *order) {
+// No atomics here: the slot inside the tile came with the count.
+__global__ void tile_scatter_kernel(const int32_t *keys, const int32_t *ranks, int64_t nq,
+                                    const int32_t *tile_start, int32_t *order) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nq;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        const int32_t key = keys[i];
-        order[tile_start[key] + atomicAdd(&cursor[key], 1)] = (int32_t)i;
-    }
+         i += (int64_t)gridDim.x * blockDim.x)
+        order[tile_start[keys[i]] + ranks[i]] = (int32_t)i;
 }
 
 size_t a256(size_t b) { return (b + 255) & ~(size_t)255; }
@@ -1206,21 +1205,20 @@ int32_t tile2d_run(const ghn_index_view *ix, const Tile2dPlan *plan, const void 
     int32_t *order = (int32_t *)(ws + q4);
     int32_t *fbl = (int32_t *)(ws + 2 * q4);
     int32_t *tstart = (int32_t *)(ws + 3 * q4);
-    int32_t *cursor = (int32_t *)(ws + 3 * q4 + t4);
+    int32_t *ranks = fbl;   // the fallback list is written only by the predict kernel, later
     int32_t *fbc = (int32_t *)(ws + 3 * q4 + 2 * t4);
     char *sws = ws + 3 * q4 + 3 * t4;
     GHN_CUDA_CHECK(cudaMemsetAsync(tstart, 0, (size_t)(plan->ntiles + 1) * 4, s));
-    GHN_CUDA_CHECK(cudaMemsetAsync(cursor, 0, (size_t)(plan->ntiles + 1) * 4, s));
     GHN_CUDA_CHECK(cudaMemsetAsync(fbc, 0, 4, s));
     unsigned g = (unsigned)((nq + 255) / 256);
     if (g > 148 * 16) g = 148 * 16;
     tile_key_kernel<<<g, 256, 0, s>>>(Q, q_dtype, nq, ix->widths[0], ix->widths[1], inv_w[0], inv_w[1],
                                       pow2, ix->lo[0], ix->lo[1], (int32_t)ix->ext[0],
-                                      (int32_t)ix->ext[1], plan->T, plan->nt1, keys, tstart);
+                                      (int32_t)ix->ext[1], plan->T, plan->nt1, keys, ranks, tstart);
     GHN_LAUNCH_CHECK("tile_key_kernel");
     int32_t rc = exclusive_scan_i32(tstart, tstart, plan->ntiles + 1, sws, s);
     if (rc) return rc;
-    tile_scatter_kernel<<<g, 256, 0, s>>>(keys, nq, tstart, cursor, order);
+    tile_scatter_kernel<<<g, 256, 0, s>>>(keys, ranks, nq, tstart, order);
     GHN_LAUNCH_CHECK("tile_scatter_kernel");
     T2Args a;
     memset(&a, 0, sizeof(a));
