@@ -768,19 +768,23 @@ __device__ __forceinline__ void run_rounds_thr(const T2Args &a, const ThrWin &w,
 // ---------------------------------------------------------------- k > 32
 // Bucket select (k in (32, 255]): the bubble's cost grows with k, so for
 // large k block(l*) is passed over twice in lock-step.  Pass 1 histograms
-// the packed keys into SB_NB buckets of 1/16 octave (packed >> 17: exponent
-// and 4 mantissa bits -- bucket edges are d-part edges) around the expected
-// k-th key, in a per-lane byte histogram in shared memory; the bucket bb
-// where the count reaches k follows.  Pass 2 votes every candidate below bb
-// and bubbles the bucket-bb candidates into a list of SB_C + 1: the k-th is
-// its r-th entry (r = k - count below bb).  Later shells are checked
-// compare-only; a later layer that changes the top-k, a boundary bucket
-// holding the k-th beyond SB_C, or a wrapped byte counter sends the
-// query to the generic kernel.  Byte counters may wrap beyond 255 points in
-// one bucket: pass 2 recounts the buckets up to bb and falls back on a
-// mismatch.
+// the packed keys (pass 1 from fp32 keys: the same bucket edges) into SB_NB
+// buckets of 2^-SB_MB octave (packed >> SB_S: exponent and SB_MB mantissa
+// bits -- bucket edges are d-part edges) around the expected k-th key, in a
+// per-lane byte histogram in shared memory; the bucket bb where the count
+// reaches k follows.  Pass 2 (exact keys) votes every candidate below bb and
+// bubbles the bucket-bb candidates into a list of SB_C + 1: the k-th is its
+// r-th entry (r = k - exact count below bb).  Later shells are checked
+// compare-only; a shell that changes the top-k makes its block the next
+// select (for >= SB_REDO lanes of the warp; a lone one goes to the generic
+// kernel), as does a boundary bucket holding the k-th beyond SB_C.  Pass 1's
+// counts are approximate (fp32 keys near an edge, byte counters that wrap
+// beyond 255): pass 2's exact counts must still put the k-th in bb.
 constexpr int SB_NB = 64;   // buckets (0 and SB_NB-1 catch the tails)
-constexpr int SB_S = 17;    // packed >> SB_S: 16 buckets per octave
+#ifndef SB_MB
+#define SB_MB 5             // mantissa bits in a bucket index: 2^SB_MB buckets per octave (4: -2 %)
+#endif
+constexpr int SB_S = 21 - SB_MB;   // packed >> SB_S: exponent + SB_MB mantissa bits
 constexpr int SB_C = 8;     // boundary list capacity
 constexpr int SB_REDO = 8;  // fewest lanes of a warp re-selecting over a larger block
 
@@ -792,12 +796,13 @@ __device__ __forceinline__ int sb_bucket(uint32_t pk, int bbase) {
 // reals (exponent + 4 mantissa bits; the fp64 index = fp32 index + (1023 -
 // 127) * 16).  The fp32 key is within a few ulps of the exact key, so the
 // bucket is exact unless the key lies within 8 ulps of an edge (`edge`).
-constexpr int SB_F32_SHIFT = (1023 - 127) * 16;
+constexpr int SB_F32_SHIFT = (1023 - 127) << SB_MB;
 __device__ __forceinline__ int sb_bucket32(float2 c, float q0f, float q1f, int bbase, bool &edge) {
     const float dx = c.x - q0f, dy = c.y - q1f;
     const uint32_t bits = __float_as_uint(__fmaf_rn(dy, dy, dx * dx));
-    edge = ((bits + 8u) & 0x7ffffu) < 16u;
-    return min(max((int)(bits >> 19) + SB_F32_SHIFT - bbase, 0), SB_NB - 1);
+    constexpr uint32_t M = (1u << (23 - SB_MB)) - 1u;
+    edge = ((bits + 8u) & M) < 16u;
+    return min(max((int)(bits >> (23 - SB_MB)) + SB_F32_SHIFT - bbase, 0), SB_NB - 1);
 }
 
 template <bool STATS>
@@ -906,12 +911,13 @@ __device__ __forceinline__ void run_rounds_sel(const T2Args &a, const ThrWin &w,
         double upper = 0.0;
         const RectBound rb0 = live ? RectBound(a, q0, q1, cc0, cc1) : RectBound();
         while (__any_sync(GHN_FULL, need)) {
-            // expected k-th key from the block's density: buckets cover [K/4, ~4K)
+            // expected k-th key from the block's density
             int bbase = 0;
             if (need) {
                 const double side = (double)(2 * ls + 1);
                 const double kest = (double)k * side * side * a.w0 * a.w1 / (3.14159265358979 * (double)cnt);
-                const double klo = kest * 0.25;
+                // the 62 inner buckets span 62 / 2^SB_MB octaves centred on kest
+                const double klo = kest * exp2(-0.5 * (SB_NB - 2) / (double)(1 << SB_MB));
                 const uint32_t top = __funnelshift_l((uint32_t)__double2loint(klo), (uint32_t)__double2hiint(klo), 1);
                 bbase = (int)(top >> SB_S) - 1;
             }
