@@ -18,3 +18,8 @@ for K in 1 4 16 64; do
       --clock-control none -k regex:'tile2d|query_kernel' --csv --log-file $O/traffic_k$K.csv $CMD > $O/ncu_tr$K.log 2>&1
   echo "traffic k=$K rc=$?"
 done
+# fit launch list (cold-cache, serialised): build the cfg4 index twice, the second is the one to read
+timeout 120 python tools/fit_launches.py > $O/fl_plain.log 2>&1 && \
+ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
+    --log-file $O/fit_launches.csv python tools/fit_launches.py > $O/fl_ncu.log 2>&1
+echo "fit launch list rc=$?"
