@@ -319,11 +319,12 @@ constexpr int FAST_MAX_CELL = 256;
 
 // X is streamed (evict-first) so the L2 keeps the per-cell counters / cursors
 // that the atomics hit.
-template <typename T>
+template <typename T, bool STREAM = true>
 __device__ __forceinline__ uint32_t point_key(const T *__restrict__ X, int64_t i, const DimParams &p) {
     uint64_t key = 0;
     for (int j = 0; j < p.d; ++j) {
-        const int64_t c = cell_id(to_double(__ldcs(X + i * p.d + j)), p.w[j], p.inv[j], (p.pow2 >> j) & 1u);
+        const T x = STREAM ? __ldcs(X + i * p.d + j) : X[i * p.d + j];
+        const int64_t c = cell_id(to_double(x), p.w[j], p.inv[j], (p.pow2 >> j) & 1u);
         key = key * (uint64_t)p.ext[j] + (uint64_t)(c - p.lo[j]);
     }
     return (uint32_t)key;
@@ -384,15 +385,28 @@ __global__ void __launch_bounds__(FIT_THREADS) scatter_records_kernel(
 // Locality pass before the cell scatter: a partition of the points by the
 // high bits of their cell key (<= 1024 key-range buckets, 4 rows of cells at
 // cfg4; measured against 256 and 4096: fewer buckets widen the scatter's
-// write window beyond L2, more shorten the partition's write runs).  Each CTA takes a contiguous chunk of points,
+// write window beyond L2, more shorten the partition's write runs).  Each CTA
+// takes a contiguous chunk of points (8K: 512 threads x 16; the counting
+// phase loads X through L2 so the writing phase re-reads it from there --
+// cfg4 fit 7.75 -> 7.3 ms against 64K-point chunks with streamed loads; 16-byte
+// cell records instead of 32 measured 7.7 ms, tools/fit_sweep.sh),
 // counts its buckets in shared memory, reserves one range per bucket with a
 // single global atomic, and writes compact records (coords, label, index)
 // into those ranges.  The cell scatter that follows then walks the points
 // bucket by bucket: its cursor atomics and its record writes stay inside one
 // bucket's window (L2-resident) instead of hitting all of HBM at random.
 constexpr int PART_BUCKETS = 1024;
-constexpr int PART_THREADS = 1024;
-constexpr int PART_CHUNK = 64 * PART_THREADS;
+#ifndef PART_THR
+#define PART_THR 512
+#endif
+constexpr int PART_THREADS = PART_THR;
+#ifndef PART_CHUNK_K
+#define PART_CHUNK_K 16
+#endif
+#ifndef PART_P1_STREAM
+#define PART_P1_STREAM 0
+#endif
+constexpr int PART_CHUNK = PART_CHUNK_K * PART_THREADS;
 
 template <typename T, int RWP>
 __global__ void __launch_bounds__(PART_THREADS) partition_kernel(const T *__restrict__ X, int64_t n, DimParams p,
@@ -405,7 +419,7 @@ __global__ void __launch_bounds__(PART_THREADS) partition_kernel(const T *__rest
     const int64_t i1 = i0 + PART_CHUNK < n ? i0 + PART_CHUNK : n;
     for (int b = threadIdx.x; b < PART_BUCKETS; b += blockDim.x) cnt[b] = 0;
     __syncthreads();
-    for (int64_t i = i0 + threadIdx.x; i < i1; i += blockDim.x) atomicAdd(&cnt[point_key(X, i, p) >> shift], 1);
+    for (int64_t i = i0 + threadIdx.x; i < i1; i += blockDim.x) atomicAdd(&cnt[point_key<T, PART_P1_STREAM>(X, i, p) >> shift], 1);
     __syncthreads();
     for (int b = threadIdx.x; b < PART_BUCKETS; b += blockDim.x) {
         const int c = cnt[b];
