@@ -346,6 +346,37 @@ __global__ void __launch_bounds__(FIT_THREADS) hist_kernel(const T *__restrict__
     for (; i < n; i += stride) atomicAdd(&counts[point_key(X, i, p)], 1);
 }
 
+// The same histogram with two 16-bit counters per word: half the counter
+// footprint (33 MB at cfg4), so the atomics stay in L2 instead of thrashing
+// the 67 MB int32 table out to HBM.  A cell of >= 65536 points carries into
+// its neighbour (or out of the word): the decoded counts then sum to less
+// than n, which the caller checks (pt_off[E] after the scan) before redoing
+// the int32 histogram.
+template <typename T>
+__global__ void __launch_bounds__(FIT_THREADS) hist16_kernel(const T *__restrict__ X, int64_t n, DimParams p,
+                                                             uint32_t *__restrict__ packed) {
+    constexpr int BU = 4;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    for (; i + (BU - 1) * stride < n; i += BU * stride) {
+        uint32_t key[BU];
+#pragma unroll
+        for (int u = 0; u < BU; ++u) key[u] = point_key(X, i + u * stride, p);
+#pragma unroll
+        for (int u = 0; u < BU; ++u) atomicAdd(&packed[key[u] >> 1], 1u << (16 * (key[u] & 1u)));
+    }
+    for (; i < n; i += stride) {
+        const uint32_t key = point_key(X, i, p);
+        atomicAdd(&packed[key >> 1], 1u << (16 * (key & 1u)));
+    }
+}
+
+__global__ void unpack16_kernel(const uint32_t *__restrict__ packed, int64_t E, int32_t *__restrict__ counts) {
+    for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c <= E;
+         c += (int64_t)gridDim.x * blockDim.x)
+        counts[c] = c < E ? (int32_t)((packed[c >> 1] >> (16 * (c & 1))) & 0xffffu) : 0;
+}
+
 __global__ void max_count_kernel(const int32_t *__restrict__ off, int64_t E, int32_t *out) {
     int m = 0;
     for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < E;
@@ -636,18 +667,36 @@ int32_t fit_build_impl(const ghn_fit_plan *plan, const T *X, const ghn_fit_out *
     if (plan->layout == GHN_LAYOUT_DENSE && RW > 0) {
         // counting scatter: histogram into pt_off[0..E), scan in place (E+1)
         const int64_t E = plan->E;
-        GHN_CUDA_CHECK(cudaMemsetAsync(out->pt_off, 0, (size_t)(E + 1) * 4, s));
-        hist_kernel<T><<<g, FIT_THREADS, 0, s>>>(X, n, p, out->pt_off);
-        GHN_LAUNCH_CHECK("hist_kernel");
+        // 16-bit counters in the cursor region (dead until after the scan)
+        uint32_t *packed = (uint32_t *)(ws + plan->fast_cursor_off);
+        GHN_CUDA_CHECK(cudaMemsetAsync(packed, 0, (size_t)((E + 1) / 2) * 4, s));
+        hist16_kernel<T><<<g, FIT_THREADS, 0, s>>>(X, n, p, packed);
+        GHN_LAUNCH_CHECK("hist16_kernel");
+        unpack16_kernel<<<grid_for(E + 1), FIT_THREADS, 0, s>>>(packed, E, out->pt_off);
+        GHN_LAUNCH_CHECK("unpack16_kernel");
         rc = exclusive_scan_i32(out->pt_off, out->pt_off, E + 1, sws, s);
         if (rc) return rc;
         int32_t *dmax = (int32_t *)kA;
+        int32_t hres[2] = {0, 0};   // largest cell, points counted
         GHN_CUDA_CHECK(cudaMemsetAsync(dmax, 0, 4, s));
         max_count_kernel<<<grid_for(E), FIT_THREADS, 0, s>>>(out->pt_off, E, dmax);
         GHN_LAUNCH_CHECK("max_count_kernel");
-        int32_t hmax = 0;
-        GHN_CUDA_CHECK(cudaMemcpyAsync(&hmax, dmax, 4, cudaMemcpyDeviceToHost, s));
+        GHN_CUDA_CHECK(cudaMemcpyAsync(&hres[0], dmax, 4, cudaMemcpyDeviceToHost, s));
+        GHN_CUDA_CHECK(cudaMemcpyAsync(&hres[1], out->pt_off + E, 4, cudaMemcpyDeviceToHost, s));
         GHN_CUDA_CHECK(cudaStreamSynchronize(s));
+        if ((int64_t)hres[1] != n) {   // a 16-bit counter overflowed: exact int32 histogram
+            GHN_CUDA_CHECK(cudaMemsetAsync(out->pt_off, 0, (size_t)(E + 1) * 4, s));
+            hist_kernel<T><<<g, FIT_THREADS, 0, s>>>(X, n, p, out->pt_off);
+            GHN_LAUNCH_CHECK("hist_kernel");
+            rc = exclusive_scan_i32(out->pt_off, out->pt_off, E + 1, sws, s);
+            if (rc) return rc;
+            GHN_CUDA_CHECK(cudaMemsetAsync(dmax, 0, 4, s));
+            max_count_kernel<<<grid_for(E), FIT_THREADS, 0, s>>>(out->pt_off, E, dmax);
+            GHN_LAUNCH_CHECK("max_count_kernel");
+            GHN_CUDA_CHECK(cudaMemcpyAsync(&hres[0], dmax, 4, cudaMemcpyDeviceToHost, s));
+            GHN_CUDA_CHECK(cudaStreamSynchronize(s));
+        }
+        const int32_t hmax = hres[0];
         if (hmax <= FAST_MAX_CELL) {
             int32_t *cursor = (int32_t *)(ws + plan->fast_cursor_off);
             uint32_t *rec = (uint32_t *)(ws + plan->fast_rec_off);

@@ -93,6 +93,25 @@ def test_duplicate_points_fall_back_exactly(ghn):
         _check_predict(ghn, index, ref, X, y, Q, k, "heuristic")
 
 
+def test_cell_over_16bit_count_exact(ghn):
+    """A cell of >= 65,536 points overflows the fit's packed 16-bit histogram
+    into its neighbour's counter; the build must detect it (counts summing to
+    less than n), recount in int32 and keep the reference's stable bucket
+    order (lexsort of the cell ids, then the input index)."""
+    rng = np.random.default_rng(11)
+    X = rng.random((240_000, 2), dtype=np.float32)
+    X[::3] = X[4]                          # 80k copies: one cell of > 65,535 points
+    X[1::3][:10_000] = X[5]                # and the next even/odd partner filled too
+    y = rng.integers(0, 4, X.shape[0]).astype(np.int32)
+    index = ghn.build_arrays(X, y, cells_per_axis=256)
+    ids = np.floor(X.astype(np.float64) * 256).astype(np.int64)
+    order = np.lexsort((np.arange(X.shape[0]), ids[:, 1], ids[:, 0]))
+    np.testing.assert_array_equal(index.perm.cpu().numpy(), order)
+    Q = np.concatenate([rng.random((20_000, 2), dtype=np.float32), np.repeat(X[4:5], 50, 0)])
+    ref = oracle.COracle(X, np.full(2, 1.0 / 256))
+    _check_predict(ghn, index, ref, X, y, Q, 8, "heuristic")
+
+
 @pytest.mark.parametrize("cfg,nq", [(1, 30_000), (2, 400)])
 def test_cfg1_cfg2_generic_kernel(ghn, cfg, nq):
     from paper_2004_02290_b200 import datagen
