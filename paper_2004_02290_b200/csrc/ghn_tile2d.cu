@@ -1127,7 +1127,7 @@ bool tile2d_plan(const ghn_index_view *ix, int64_t nq, int32_t k, int32_t task, 
     if (ix->density_hint > rho) rho = ix->density_hint;
     int lf = 0;
     while (lf < 8 && (2.0 * lf + 1) * (2.0 * lf + 1) * rho < (double)k) ++lf;
-    const int A = lf + 2 > 4 ? 4 : lf + 2;
+    const int A = getenv("GHN_TILE_A") ? atoi(getenv("GHN_TILE_A")) : (lf + 2 > 4 ? 4 : lf + 2);   // env: measurement knob
     int T = (int)floor(sqrt(0.7 * T2_CAP / (rho > 1e-9 ? rho : 1e-9))) - 2 * A;
     const double Tmax = sqrt((double)ix->E / (148.0 * 4.0));
     if (T > Tmax) T = (int)Tmax;
