@@ -57,28 +57,54 @@ __global__ void __launch_bounds__(SCAN_THREADS) scan_reduce_kernel(const int32_t
     }
 }
 
+// VEC: a thread's 8 elements move as two 16-byte words (in / out 16-byte
+// aligned; full tiles only -- the caller routes the tail tile to VEC=false).
+template <bool VEC>
 __global__ void __launch_bounds__(SCAN_THREADS) scan_downsweep_kernel(const int32_t *in, int32_t *out,
                                                                       int64_t len,
-                                                                      const int32_t *partials) {
-    const int64_t base = (int64_t)blockIdx.x * SCAN_TILE + (int64_t)threadIdx.x * SCAN_IPT;
+                                                                      const int32_t *partials,
+                                                                      int64_t tile0 = 0) {
+    const int64_t tile = tile0 + blockIdx.x;
+    const int64_t base = tile * SCAN_TILE + (int64_t)threadIdx.x * SCAN_IPT;
     int v[SCAN_IPT];
     int s = 0;
+    if (VEC) {
+        const int4 a = reinterpret_cast<const int4 *>(in + base)[0];
+        const int4 b = reinterpret_cast<const int4 *>(in + base)[1];
+        v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+        v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
 #pragma unroll
-    for (int i = 0; i < SCAN_IPT; ++i) {
-        int64_t e = base + i;
-        v[i] = e < len ? in[e] : 0;
-        s += v[i];
+        for (int i = 0; i < SCAN_IPT; ++i) s += v[i];
+    } else {
+#pragma unroll
+        for (int i = 0; i < SCAN_IPT; ++i) {
+            int64_t e = base + i;
+            v[i] = e < len ? in[e] : 0;
+            s += v[i];
+        }
     }
     int total;
     int ex = block_exclusive_scan(s, &total);
-    int run = ex + (partials ? partials[blockIdx.x] : 0);
+    int run = ex + (partials ? partials[tile] : 0);
+    if (VEC) {
+        int r[SCAN_IPT];
 #pragma unroll
-    for (int i = 0; i < SCAN_IPT; ++i) {
-        int64_t e = base + i;
-        if (e < len) out[e] = run;
-        run += v[i];
+        for (int i = 0; i < SCAN_IPT; ++i) {
+            r[i] = run;
+            run += v[i];
+        }
+        reinterpret_cast<int4 *>(out + base)[0] = make_int4(r[0], r[1], r[2], r[3]);
+        reinterpret_cast<int4 *>(out + base)[1] = make_int4(r[4], r[5], r[6], r[7]);
+    } else {
+#pragma unroll
+        for (int i = 0; i < SCAN_IPT; ++i) {
+            int64_t e = base + i;
+            if (e < len) out[e] = run;
+            run += v[i];
+        }
     }
 }
+static_assert(SCAN_IPT == 8, "the VEC downsweep moves 8 elements per thread");
 }  // namespace
 
 static int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
@@ -97,7 +123,7 @@ int32_t exclusive_scan_i32(const int32_t *in, int32_t *out, int64_t len, void *w
     if (len <= 0) return GHN_OK;
     int64_t nb = ceil_div(len, SCAN_TILE);
     if (nb == 1) {
-        scan_downsweep_kernel<<<1, SCAN_THREADS, 0, s>>>(in, out, len, nullptr);
+        scan_downsweep_kernel<false><<<1, SCAN_THREADS, 0, s>>>(in, out, len, nullptr);
         GHN_LAUNCH_CHECK("scan_downsweep_kernel");
         return GHN_OK;
     }
@@ -107,7 +133,17 @@ int32_t exclusive_scan_i32(const int32_t *in, int32_t *out, int64_t len, void *w
     GHN_LAUNCH_CHECK("scan_reduce_kernel");
     int32_t rc = exclusive_scan_i32(partials, partials, nb, ws_next, s);
     if (rc != GHN_OK) return rc;
-    scan_downsweep_kernel<<<(unsigned)nb, SCAN_THREADS, 0, s>>>(in, out, len, partials);
+    const int64_t full = len / SCAN_TILE;   // complete tiles
+    if ((((uintptr_t)in | (uintptr_t)out) & 15) == 0 && full > 0) {
+        scan_downsweep_kernel<true><<<(unsigned)full, SCAN_THREADS, 0, s>>>(in, out, len, partials);
+        GHN_LAUNCH_CHECK("scan_downsweep_kernel");
+        if (full < nb) {
+            scan_downsweep_kernel<false><<<(unsigned)(nb - full), SCAN_THREADS, 0, s>>>(in, out, len, partials, full);
+            GHN_LAUNCH_CHECK("scan_downsweep_kernel");
+        }
+        return GHN_OK;
+    }
+    scan_downsweep_kernel<false><<<(unsigned)nb, SCAN_THREADS, 0, s>>>(in, out, len, partials);
     GHN_LAUNCH_CHECK("scan_downsweep_kernel");
     return GHN_OK;
 }
