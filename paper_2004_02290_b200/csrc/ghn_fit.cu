@@ -575,10 +575,20 @@ __global__ void cells_from_offsets_kernel(const int32_t *__restrict__ pt_off,
         if (pt_off[c + 1] > pt_off[c]) {
             const int32_t idx = ne_off[c];
             cell_start[idx] = pt_off[c];
-            uint64_t rem = (uint64_t)c;
-            for (int j = d - 1; j >= 0; --j) {
-                cell_ids[(int64_t)idx * d + j] = (int32_t)(rem % (uint64_t)p.ext[j]);
-                rem /= (uint64_t)p.ext[j];
+            if (E <= 0xffffffffLL) {   // 32-bit divisions (the 64-bit ones are a software loop)
+                uint32_t rem = (uint32_t)c;
+                for (int j = d - 1; j >= 0; --j) {
+                    const uint32_t e = (uint32_t)p.ext[j];
+                    const uint32_t q = rem / e;
+                    cell_ids[(int64_t)idx * d + j] = (int32_t)(rem - q * e);
+                    rem = q;
+                }
+            } else {
+                uint64_t rem = (uint64_t)c;
+                for (int j = d - 1; j >= 0; --j) {
+                    cell_ids[(int64_t)idx * d + j] = (int32_t)(rem % (uint64_t)p.ext[j]);
+                    rem /= (uint64_t)p.ext[j];
+                }
             }
         }
         if (c == 0) {
