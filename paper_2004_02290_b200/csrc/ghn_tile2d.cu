@@ -78,7 +78,7 @@ struct T2Args {
     int32_t dbg;
     int32_t small_labels;
     int32_t lmask;   // label-code mask of the thread kernel (2^LB - 1)
-    int32_t sb_capn, sb_redo, sb_wmax, sb_sort;   // bucket-select lock-step knobs (see ghn_tile2d_thr.cuh)
+    int32_t sb_capn, sb_redo, sb_wmax, sb_sort, sb_recap;   // bucket-select lock-step knobs (see ghn_tile2d_thr.cuh)
     double tt_skipf;   // k = 3, 4 rounds: skip-ahead threshold (fraction of the block half-width)
 };
 
@@ -565,6 +565,15 @@ __device__ __forceinline__ int32_t vote_tiebreak_c(const T2Args &a, const Cands 
     }
     return bl;
 }
+
+// Diagnostics build (-DGHN_FB_REASONS): per-site counts of the thread
+// kernel's bucket-select fallbacks, printed under GHN_DEBUG_FALLBACK.
+#ifdef GHN_FB_REASONS
+__device__ unsigned long long g_fb_reason[16];
+#define FB_REASON(r) atomicAdd(&g_fb_reason[r], 1ull)
+#else
+#define FB_REASON(r) ((void)0)
+#endif
 
 __device__ __forceinline__ void push_fallback(const T2Args &a, int32_t qi) {
     const int32_t slot = atomicAdd(a.fb_count, 1);
@@ -1261,6 +1270,7 @@ int32_t tile2d_run(const ghn_index_view *ix, const Tile2dPlan *plan, const void 
     a.lmask = ix->n_labels <= 2 ? 1 : (ix->n_labels <= 4 ? 3 : 7);
     a.sb_capn = getenv("GHN_SB_CAPN") ? atoi(getenv("GHN_SB_CAPN")) : 255;
     a.sb_redo = getenv("GHN_SB_REDO") ? atoi(getenv("GHN_SB_REDO")) : 2;
+    a.sb_recap = getenv("GHN_SB_RECAP") ? atoi(getenv("GHN_SB_RECAP")) : 255;   // > 255: 11.47 vs 11.03 ms at cfg4 k=64
     a.sb_wmax = getenv("GHN_SB_WMAX") ? atoi(getenv("GHN_SB_WMAX")) : 0;
     a.sb_sort = getenv("GHN_SB_SORT") ? atoi(getenv("GHN_SB_SORT")) : 1;
     a.tt_skipf = getenv("GHN_TT_SKIPF") ? atof(getenv("GHN_TT_SKIPF")) : 0.4;
@@ -1317,6 +1327,13 @@ int32_t tile2d_run(const ghn_index_view *ix, const Tile2dPlan *plan, const void 
         cudaMemcpyAsync(&nfb, fbc, 4, cudaMemcpyDeviceToHost, s);
         cudaStreamSynchronize(s);
         fprintf(stderr, "[ghn] tile2d k=%d nq=%lld fallbacks=%d\n", k, (long long)nq, nfb);
+#ifdef GHN_FB_REASONS
+        unsigned long long r[16];
+        cudaMemcpyFromSymbol(r, g_fb_reason, sizeof(r));
+        fprintf(stderr, "[ghn] fallback sites (cumulative):");
+        for (int i = 0; i < 16; ++i) if (r[i]) fprintf(stderr, " %d:%llu", i, r[i]);
+        fprintf(stderr, "\n");
+#endif
     }
     *fb_list = fbl;
     *fb_count = fbc;

@@ -845,7 +845,7 @@ __device__ __forceinline__ void run_rounds_sel(const T2Args &a, const ThrWin &w,
             cc1 = cell_id(q1, a.w1, a.inv1, (a.pow2 >> 1) & 1u) - a.lo1;
             if (cc0 < tr0 || cc0 >= tr0 + a.T || cc1 < tc0 || cc1 >= tc0 + a.T || cc0 >= a.ext0 ||
                 cc1 >= a.ext1) {
-                push_fallback(a, qi);
+                { FB_REASON(1); push_fallback(a, qi); }
                 live = false;
             }
         }
@@ -855,7 +855,7 @@ __device__ __forceinline__ void run_rounds_sel(const T2Args &a, const ThrWin &w,
             lmax = max(max((int)cc0, a.ext0 - 1 - (int)cc0), max((int)cc1, a.ext1 - 1 - (int)cc1));
             for (;;) {
                 if (l > a.A) {
-                    push_fallback(a, qi);
+                    { FB_REASON(2); push_fallback(a, qi); }
                     live = false;
                     break;
                 }
@@ -964,8 +964,20 @@ __device__ __forceinline__ void run_rounds_sel(const T2Args &a, const ThrWin &w,
                         cum += c;
                     }
                 }
-                if (!found || k - below > SB_C) {   // wrapped counts, or the k-th too deep in its bucket
-                    push_fallback(a, qi);
+                // more than 255 candidates: a byte counter may have carried
+                // into its neighbour (or out of the word); each carry loses
+                // >= 255 from the decoded total, so the total is exact iff none did
+                bool wrap = false;
+                if (n > 255) {
+                    int tot = 0;
+                    for (int i = 0; i < SB_NB / 4; ++i) {
+                        const uint32_t wd = myh[i * TT_THREADS];
+                        tot += (int)((wd & 0xffu) + ((wd >> 8) & 0xffu) + ((wd >> 16) & 0xffu) + (wd >> 24));
+                    }
+                    wrap = tot != n;
+                }
+                if (!found || wrap || k - below > SB_C) {   // wrapped counts, or the k-th too deep in its bucket
+                    { FB_REASON(3); push_fallback(a, qi); }
                     sel = false;
                 }
             }
@@ -1034,7 +1046,7 @@ __device__ __forceinline__ void run_rounds_sel(const T2Args &a, const ThrWin &w,
                     if (b2 >= upper) stop = true;
                     else if (b2 > thr_lower(tm)) bad = true;
                 }
-                if (bad) push_fallback(a, qi);
+                if (bad) { FB_REASON(4); push_fallback(a, qi); }
                 else if (stop || l >= lmax) fin = true;
                 else more = true;
             }
@@ -1043,7 +1055,7 @@ __device__ __forceinline__ void run_rounds_sel(const T2Args &a, const ThrWin &w,
                 if (more) {
                     ++l;
                     if (l > a.A) {
-                        push_fallback(a, qi);
+                        { FB_REASON(5); push_fallback(a, qi); }
                         more = false;
                     }
                 }
@@ -1077,7 +1089,7 @@ __device__ __forceinline__ void run_rounds_sel(const T2Args &a, const ThrWin &w,
                     }
                 }
                 if (more && eq) {   // undecidable d-part
-                    push_fallback(a, qi);
+                    { FB_REASON(6); push_fallback(a, qi); }
                     more = false;
                 }
                 if (more) {
@@ -1096,7 +1108,7 @@ __device__ __forceinline__ void run_rounds_sel(const T2Args &a, const ThrWin &w,
                             if (b2 >= upper) {
                                 stop = true;
                             } else if (b2 > thr_lower(tm)) {
-                                push_fallback(a, qi);
+                                { FB_REASON(7); push_fallback(a, qi); }
                                 more = false;
                             }
                         }
@@ -1110,8 +1122,8 @@ __device__ __forceinline__ void run_rounds_sel(const T2Args &a, const ThrWin &w,
             // a lone re-select would hold the whole warp for a block's worth
             // of steps: below SB_REDO lanes the generic kernel is cheaper
             const int nredo = __popc(__ballot_sync(GHN_FULL, need));
-            if (need && (nredo < a.sb_redo || cnt > a.sb_capn)) {
-                push_fallback(a, qi);
+            if (need && (nredo < a.sb_redo || cnt > a.sb_recap)) {
+                { FB_REASON(8); push_fallback(a, qi); }
                 need = false;
             }
         }
@@ -1165,7 +1177,7 @@ __device__ __forceinline__ void run_rounds_sel(const T2Args &a, const ThrWin &w,
                         w2 = min(w2, mn[j]);
                 const int lbits = __popc(fmask);
                 if ((w2 >> lbits) - (w1 >> lbits) < 2u) {
-                    push_fallback(a, qi);
+                    { FB_REASON(9); push_fallback(a, qi); }
                     fin = false;
                 } else {
                     wl = (int)(w1 & lmask);

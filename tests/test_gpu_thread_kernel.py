@@ -70,6 +70,17 @@ def test_bucket_select_for_small_k(ghn, case, k, monkeypatch):
     _check(ghn, index, ref, w.y, w.Q[:20000], k, "heuristic")
 
 
+@pytest.mark.parametrize("k", [40, 64, 100])
+@pytest.mark.parametrize("mode", ["heuristic", "guaranteed"])
+def test_reselect_over_255_candidates(ghn, case, k, mode, monkeypatch):
+    """Re-selects over more than 255 candidates (GHN_SB_RECAP raised): the
+    byte histogram may carry between buckets; the decoded-total check must
+    send exactly those queries to the generic kernel, the rest stay exact."""
+    monkeypatch.setenv("GHN_SB_RECAP", "4095")
+    w, index, ref = case
+    _check(ghn, index, ref, w.y, w.Q[:20000], k, mode)
+
+
 @pytest.mark.parametrize("n_labels", [2, 8])
 @pytest.mark.parametrize("k", [1, 16, 64])
 def test_label_codes_2_and_8(ghn, n_labels, k):
