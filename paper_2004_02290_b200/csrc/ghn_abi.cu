@@ -2,6 +2,7 @@
 #include <atomic>
 #include <stdarg.h>
 #include <stdio.h>
+#include <stdlib.h>
 
 #include "ghn_common.cuh"
 
@@ -18,6 +19,29 @@ void set_error(const char *fmt, ...) {
     vsnprintf(g_last_error, sizeof(g_last_error), fmt, ap);
     va_end(ap);
 }
+
+// Streaming multiprocessors of the current device (grid sizing), cached per
+// device; 148 on B200.
+int sm_count() {
+    static std::atomic<int> cache[64];
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0) return 148;
+    if (dev < 64) {
+        const int c = cache[dev].load(std::memory_order_relaxed);
+        if (c > 0) return c;
+    }
+    int v = 0;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0) return 148;
+    if (dev < 64) cache[dev].store(v, std::memory_order_relaxed);
+    return v;
+}
+
+#ifdef GHN_TUNING_KNOBS
+double knob(const char *name, double dflt) {
+    const char *e = getenv(name);
+    return e ? atof(e) : dflt;
+}
+#endif
 
 int32_t cuda_status(cudaError_t e, const char *where) {
     set_error("CUDA error in %s: %s", where, cudaGetErrorString(e));

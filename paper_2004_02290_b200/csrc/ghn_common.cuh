@@ -21,6 +21,15 @@ int32_t cuda_status(cudaError_t e, const char *where);
     } while (0)
 
 void count_launch();
+int sm_count();   // SMs of the current device (cached)
+
+// Measurement knobs: environment overrides exist only in a tuning build
+// (-DGHN_TUNING_KNOBS); the product library always uses the defaults.
+#ifdef GHN_TUNING_KNOBS
+double knob(const char *name, double dflt);
+#else
+inline double knob(const char *, double dflt) { return dflt; }
+#endif
 
 #define GHN_LAUNCH_CHECK(where)                                        \
     do {                                                               \

@@ -626,7 +626,7 @@ static size_t fast_bcur_off(const ghn_fit_plan *plan) {
 
 static unsigned grid_for(int64_t n, int threads = FIT_THREADS) {
     int64_t b = (n + threads - 1) / threads;
-    int64_t cap = 148LL * 16;
+    int64_t cap = (int64_t)sm_count() * 16;
     if (b > cap) b = cap;
     if (b < 1) b = 1;
     return (unsigned)b;

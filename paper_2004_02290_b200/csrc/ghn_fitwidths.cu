@@ -132,7 +132,7 @@ size_t a256(size_t b) { return (b + 255) & ~(size_t)255; }
 
 unsigned grid_of(int64_t n) {
     int64_t b = (n + FW_THREADS - 1) / FW_THREADS;
-    if (b > 148 * 16) b = 148 * 16;
+    if (b > sm_count() * 16) b = sm_count() * 16;
     return (unsigned)(b < 1 ? 1 : b);
 }
 

@@ -581,35 +581,27 @@ __global__ void __launch_bounds__(Q_THREADS, KS <= 2 ? 5 : (KS == 4 ? 3 : 2)) qu
 }
 
 // ------------------------------------------------------------ query binning
-template <typename T>
-__global__ void query_bin_key_kernel(const T *__restrict__ Q, int64_t nq, int d, const double *w,
-                                     const double *inv, uint32_t pow2, const int64_t *lo,
-                                     const int64_t *ext, int drop, uint32_t *keys) {
-    __shared__ double sw[GHN_MAX_DIM], sinv[GHN_MAX_DIM];
-    __shared__ int64_t slo[GHN_MAX_DIM], sext[GHN_MAX_DIM];
-    if (threadIdx.x < d) {
-        sw[threadIdx.x] = w[threadIdx.x];
-        sinv[threadIdx.x] = inv[threadIdx.x];
-        slo[threadIdx.x] = lo[threadIdx.x];
-        sext[threadIdx.x] = ext[threadIdx.x];
-    }
-    __syncthreads();
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nq;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        uint64_t key = 0;
-        for (int j = 0; j < d; ++j) {
-            int64_t c = cell_id(to_double(Q[i * d + j]), sw[j], sinv[j], (pow2 >> j) & 1u) - slo[j];
-            c = c < 0 ? 0 : (c >= sext[j] ? sext[j] - 1 : c);
-            key = key * (uint64_t)sext[j] + (uint64_t)c;
-        }
-        keys[i] = (uint32_t)(key >> drop);
-    }
-}
-
 struct BinConsts {
     double w[GHN_MAX_DIM], inv[GHN_MAX_DIM];
     int64_t lo[GHN_MAX_DIM], ext[GHN_MAX_DIM];
 };
+
+// The grid constants travel as a kernel parameter (512 B): no H2D copy, so
+// binning never synchronises the stream with the host.
+template <typename T>
+__global__ void query_bin_key_kernel(const T *__restrict__ Q, int64_t nq, int d, const BinConsts bc,
+                                     uint32_t pow2, int drop, uint32_t *keys) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nq;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        uint64_t key = 0;
+        for (int j = 0; j < d; ++j) {
+            int64_t c = cell_id(to_double(Q[i * d + j]), bc.w[j], bc.inv[j], (pow2 >> j) & 1u) - bc.lo[j];
+            c = c < 0 ? 0 : (c >= bc.ext[j] ? bc.ext[j] - 1 : c);
+            key = key * (uint64_t)bc.ext[j] + (uint64_t)c;
+        }
+        keys[i] = (uint32_t)(key >> drop);
+    }
+}
 
 static size_t a256(size_t b) { return (b + 255) & ~(size_t)255; }
 
@@ -623,7 +615,7 @@ constexpr int64_t BIN_MIN_QUERIES = 2048;
 
 template <typename T, int D>
 int32_t launch_query_d(const QArgs &a, int ks, cudaStream_t s) {
-    int64_t g = a.nq_dev ? 148LL * 8 : (a.nq + Q_WARPS - 1) / Q_WARPS;
+    int64_t g = a.nq_dev ? (int64_t)sm_count() * 8 : (a.nq + Q_WARPS - 1) / Q_WARPS;
     if (g > 0x7fffffffLL) g = 0x7fffffffLL;
     const unsigned grid = (unsigned)g;
     switch (ks) {
@@ -723,8 +715,6 @@ extern "C" int32_t ghn_query_order(const ghn_index_view *ix, const void *Q, int3
         bc.lo[j] = ix->lo[j];
         bc.ext[j] = ix->ext[j];
     }
-    BinConsts *dbc = (BinConsts *)ws;
-    GHN_CUDA_CHECK(cudaMemcpyAsync(dbc, &bc, sizeof(bc), cudaMemcpyHostToDevice, s));
     const size_t q4 = a256((size_t)nq * 4);
     char *p = ws + a256(sizeof(BinConsts));
     uint32_t *kin = (uint32_t *)p;
@@ -737,13 +727,11 @@ extern "C" int32_t ghn_query_order(const ghn_index_view *ix, const void *Q, int3
     if (keep > 24) keep = 24;
     const int drop = kb > keep ? kb - keep : 0;
     unsigned g = (unsigned)((nq + 255) / 256);
-    if (g > 148 * 16) g = 148 * 16;
+    if (g > (unsigned)sm_count() * 16) g = (unsigned)sm_count() * 16;
     if (q_dtype == GHN_F32)
-        query_bin_key_kernel<float><<<g, 256, 0, s>>>((const float *)Q, nq, ix->d, dbc->w, dbc->inv,
-                                                     pow2, dbc->lo, dbc->ext, drop, kin);
+        query_bin_key_kernel<float><<<g, 256, 0, s>>>((const float *)Q, nq, ix->d, bc, pow2, drop, kin);
     else
-        query_bin_key_kernel<double><<<g, 256, 0, s>>>((const double *)Q, nq, ix->d, dbc->w, dbc->inv,
-                                                      pow2, dbc->lo, dbc->ext, drop, kin);
+        query_bin_key_kernel<double><<<g, 256, 0, s>>>((const double *)Q, nq, ix->d, bc, pow2, drop, kin);
     GHN_LAUNCH_CHECK("query_bin_key_kernel");
     return radix_sort_pairs(kin, nullptr, kout, order_out, ktmp, vtmp, nq, kb - drop, rws, s);
 }
@@ -810,7 +798,7 @@ extern "C" int32_t ghn_gather_i32(const int32_t *src, const int32_t *idx, int64_
                                   void *stream) {
     if (n <= 0) return GHN_OK;
     unsigned g = (unsigned)((n + 255) / 256);
-    if (g > 148 * 16) g = 148 * 16;
+    if (g > (unsigned)sm_count() * 16) g = (unsigned)sm_count() * 16;
     gather_i32_kernel<<<g, 256, 0, (cudaStream_t)stream>>>(src, idx, n, dst);
     GHN_LAUNCH_CHECK("gather_i32_kernel");
     return GHN_OK;

@@ -1119,8 +1119,7 @@ __global__ void window_density_kernel(const int32_t *__restrict__ cell_start, co
 // Largest k answered with the register list; larger k use the bucket select
 // (GHN_TT_LISTMAX overrides, for measurements).
 static int tt_list_kmax() {
-    const char *e = getenv("GHN_TT_LISTMAX");
-    return e ? atoi(e) : TT_LIST_KMAX;
+    return (int)knob("GHN_TT_LISTMAX", TT_LIST_KMAX);
 }
 
 bool tile2d_plan(const ghn_index_view *ix, int64_t nq, int32_t k, int32_t task, bool want_neighbors,
@@ -1136,9 +1135,9 @@ bool tile2d_plan(const ghn_index_view *ix, int64_t nq, int32_t k, int32_t task, 
     if (ix->density_hint > rho) rho = ix->density_hint;
     int lf = 0;
     while (lf < 8 && (2.0 * lf + 1) * (2.0 * lf + 1) * rho < (double)k) ++lf;
-    const int A = getenv("GHN_TILE_A") ? atoi(getenv("GHN_TILE_A")) : (lf + 2 > 4 ? 4 : lf + 2);   // env: measurement knob
+    const int A = (int)knob("GHN_TILE_A", lf + 2 > 4 ? 4 : lf + 2);
     int T = (int)floor(sqrt(0.7 * T2_CAP / (rho > 1e-9 ? rho : 1e-9))) - 2 * A;
-    const double Tmax = sqrt((double)ix->E / (148.0 * 4.0));
+    const double Tmax = sqrt((double)ix->E / (sm_count() * 4.0));
     if (T > Tmax) T = (int)Tmax;
     if (T > 64) T = 64;
     if (T < 1) return false;
@@ -1156,11 +1155,11 @@ bool tile2d_plan(const ghn_index_view *ix, int64_t nq, int32_t k, int32_t task, 
     if (k == 1 && ix->n_labels > 0 && ix->n_labels <= 32) plan->G = 8;
     // thread per query (packed-key register list): k <= 32, <= 8 label codes
     if (k <= TT_KMAX && ix->n_labels > 0 && ix->n_labels <= 8) plan->G = 1;
-    if (getenv("GHN_TILE_G")) plan->G = atoi(getenv("GHN_TILE_G"));
+    plan->G = (int)knob("GHN_TILE_G", plan->G);
     if (plan->G == 1) {
         // ~TT_Q queries per tile (one or two per thread) within the staging capacity
         const double qd = (double)nq / (double)ix->E;
-        const double tq = getenv("GHN_TT_Q") ? atof(getenv("GHN_TT_Q")) : TT_Q;
+        const double tq = knob("GHN_TT_Q", TT_Q);
         int Tq = (int)floor(sqrt(tq / (qd > 1e-9 ? qd : 1e-9)));
         const int Tc = (int)floor(sqrt((TT_CAP - 64.0) / 1.1 / (rho > 1e-9 ? rho : 1e-9))) - 2 * A;
         if (Tq > Tc) Tq = Tc;
@@ -1220,7 +1219,7 @@ int32_t tile2d_run(const ghn_index_view *ix, const Tile2dPlan *plan, const void 
     GHN_CUDA_CHECK(cudaMemsetAsync(tstart, 0, (size_t)(plan->ntiles + 1) * 4, s));
     GHN_CUDA_CHECK(cudaMemsetAsync(fbc, 0, 4, s));
     unsigned g = (unsigned)((nq + 255) / 256);
-    if (g > 148 * 16) g = 148 * 16;
+    if (g > (unsigned)sm_count() * 16) g = (unsigned)sm_count() * 16;
     tile_key_kernel<<<g, 256, 0, s>>>(Q, q_dtype, nq, ix->widths[0], ix->widths[1], inv_w[0], inv_w[1],
                                       pow2, ix->lo[0], ix->lo[1], (int32_t)ix->ext[0],
                                       (int32_t)ix->ext[1], plan->T, plan->nt1, keys, ranks, tstart);
@@ -1265,15 +1264,15 @@ int32_t tile2d_run(const ghn_index_view *ix, const Tile2dPlan *plan, const void 
     a.totals = out->totals;
     a.fb_list = fbl;
     a.fb_count = fbc;
-    a.dbg = getenv("GHN_DEBUG_MODE") ? atoi(getenv("GHN_DEBUG_MODE")) : 0;
+    a.dbg = (int)knob("GHN_DEBUG_MODE", 0);   // tuning builds only: 1/2 are diagnostics that overwrite labels
     a.small_labels = ix->n_labels > 0 && ix->n_labels <= 32;
     a.lmask = ix->n_labels <= 2 ? 1 : (ix->n_labels <= 4 ? 3 : 7);
-    a.sb_capn = getenv("GHN_SB_CAPN") ? atoi(getenv("GHN_SB_CAPN")) : 255;
-    a.sb_redo = getenv("GHN_SB_REDO") ? atoi(getenv("GHN_SB_REDO")) : 2;
-    a.sb_recap = getenv("GHN_SB_RECAP") ? atoi(getenv("GHN_SB_RECAP")) : 255;   // > 255: 11.47 vs 11.03 ms at cfg4 k=64
-    a.sb_wmax = getenv("GHN_SB_WMAX") ? atoi(getenv("GHN_SB_WMAX")) : 0;
-    a.sb_sort = getenv("GHN_SB_SORT") ? atoi(getenv("GHN_SB_SORT")) : 1;
-    a.tt_skipf = getenv("GHN_TT_SKIPF") ? atof(getenv("GHN_TT_SKIPF")) : 0.4;
+    a.sb_capn = (int)knob("GHN_SB_CAPN", 255);
+    a.sb_redo = (int)knob("GHN_SB_REDO", 2);
+    a.sb_recap = (int)knob("GHN_SB_RECAP", 255);   // > 255: 11.47 vs 11.03 ms at cfg4 k=64
+    a.sb_wmax = (int)knob("GHN_SB_WMAX", 0);
+    a.sb_sort = (int)knob("GHN_SB_SORT", 1);
+    a.tt_skipf = knob("GHN_TT_SKIPF", 0.4);
     const bool stats = out->stats != nullptr || out->totals != nullptr;
     // warp kernel: extraction select for small k (EXT), histogram select otherwise
     int ki = plan->G == 8 ? 1 : (plan->G == 16 ? 2 : (k >= 2 && k <= T2_EXT_MAXK ? 3 : 0));
@@ -1322,7 +1321,7 @@ int32_t tile2d_run(const ghn_index_view *ix, const Tile2dPlan *plan, const void 
     else
         tile2d_kernel<false><<<nb, T2_THREADS, plan->smem, s>>>(a);
     GHN_LAUNCH_CHECK("tile2d_kernel");
-    if (getenv("GHN_DEBUG_FALLBACK")) {   // diagnostics: queries sent to the generic kernel
+    if (knob("GHN_DEBUG_FALLBACK", 0) != 0) {   // diagnostics: queries sent to the generic kernel
         int32_t nfb = 0;
         cudaMemcpyAsync(&nfb, fbc, 4, cudaMemcpyDeviceToHost, s);
         cudaStreamSynchronize(s);

@@ -85,8 +85,15 @@ def _validate_queries(index: GridIndex, Q, k: int):
 
 def _run(index: GridIndex, Qt, k, mode, task, want_neighbors, want_stats, want_totals=False,
          stream=None, qorder=None, want_confidence=True):
+    """One ghn_query launch.  With an explicit ``stream`` every allocation,
+    conversion and the launch happen on that stream (torch.cuda.stream), so
+    the caching allocator ties the workspace and outputs to it."""
     import torch
 
+    if stream is not None:
+        with torch.cuda.stream(stream):
+            return _run(index, Qt, k, mode, task, want_neighbors, want_stats, want_totals, None, qorder,
+                        want_confidence)
     L = _lib.require_device()
     dev = index.X.device
     Qd = Qt.to(dev).contiguous()
@@ -160,6 +167,9 @@ def query_order(index: GridIndex, Q, stream=None):
     import torch
 
     L = _lib.require_device()
+    if stream is not None:
+        with torch.cuda.stream(stream):
+            return query_order(index, Q)
     Qd = torch.as_tensor(Q).to(index.X.device).contiguous()
     if Qd.dtype not in (torch.float32, torch.float64):
         Qd = Qd.to(torch.float64)

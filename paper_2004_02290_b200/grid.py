@@ -329,6 +329,11 @@ def build_arrays(X, y=None, params: GridParams | None = None, cells_per_axis=Non
 
     check_metric(metric)
     L = _lib.require_device()
+    if stream is not None:
+        # every allocation, host read and launch on the caller's stream
+        with torch.cuda.stream(stream):
+            return build_arrays(X, y, params=params, cells_per_axis=cells_per_axis, metric=metric,
+                                max_splits=max_splits)
     dev = torch.device("cuda", torch.cuda.current_device())
     Xt = torch.as_tensor(X)
     if Xt.dtype not in (torch.float32, torch.float64):
@@ -354,7 +359,7 @@ def build_arrays(X, y=None, params: GridParams | None = None, cells_per_axis=Non
         raise ValueError("params dimension does not match the data")
     Xd = Xt.to(dev).contiguous()
     dtype = _lib.GHN_F32 if Xd.dtype == torch.float32 else _lib.GHN_F64
-    s = _lib.stream_handle(stream)
+    s = _lib.stream_handle()
     widths = np.ascontiguousarray(params.widths, dtype=np.float64)
     wptr = widths.ctypes.data_as(ctypes.c_void_p)
     bounds = torch.empty(2 * d, dtype=torch.int64, device=dev)
