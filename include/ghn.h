@@ -114,6 +114,24 @@ int32_t ghn_fit_widths(const void *X, int32_t dtype, int64_t n, int32_t d, int64
  * keys_to_distances (core.py:72-91), batched over nq queries, with the
  * predict.classify / predict.regress(agg="mean") epilogue (predict.py:20-47)
  * fused. */
+/* Nested grid of one overfull cell (new; no reference counterpart).  A cell
+ * holding more than `sub_min` points is subdivided into ext[0] x ... x
+ * ext[d-1] sub-cells of width h over the bounding box of its points, so the
+ * predict can find the cell's nearest members without scanning all of them.
+ * This changes only which candidates are evaluated, never the result: every
+ * skipped sub-cell is provably farther than the current k-th key. */
+typedef struct ghn_subgrid {
+    double origin[GHN_MAX_DIM];   /* per-dimension minimum of the cell's points */
+    double h[GHN_MAX_DIM];        /* sub-cell width (> 0) */
+    double inv_h[GHN_MAX_DIM];    /* 1 / h */
+    int32_t ext[GHN_MAX_DIM];     /* sub-cells per dimension (>= 1) */
+    int64_t off;                  /* first entry of this sub-grid in sub_off */
+    int32_t cell;                 /* non-empty cell index (cell_start row) */
+    int32_t start;                /* CSR slot range of the cell: [start, start + count) */
+    int32_t count;
+    int32_t pad;
+} ghn_subgrid;
+
 typedef struct ghn_index_view {
     int64_t n;
     int32_t d;
@@ -138,6 +156,16 @@ typedef struct ghn_index_view {
     int32_t metric;              /* GHN_METRIC_*: ordering key and stop bound (core.py:72-91) */
     double density_hint;         /* points per cell the tiled predict sizes its tiles for
                                     (ghn_window_density); 0 = the mean n / E */
+    /* nested grids of overfull cells (ghn_subgrid_*), or n_sub = 0 */
+    int32_t n_sub;
+    int32_t sub_min;             /* cells with more points than this have a sub-grid */
+    const int32_t *sub_of_cell;  /* (n_cells) sub-grid id of non-empty cell c, or -1 */
+    const ghn_subgrid *subs;     /* (n_sub) */
+    const int32_t *sub_off;      /* sub-cell prefix: sub-cell t of grid g holds sub-slots
+                                    [sub_off[off_g + t], sub_off[off_g + t + 1]) */
+    const void *sub_coords;      /* SoA over n_subpts sub-slots, dtype */
+    const int32_t *sub_idx;      /* sub-slot -> original point index */
+    int64_t n_subpts;
 } ghn_index_view;
 
 typedef struct ghn_query_out {
@@ -180,6 +208,31 @@ int32_t ghn_gather_i32(const int32_t *src, const int32_t *idx, int64_t n, int32_
  * 2-D DENSE indexes only (GHN_ERR_UNSUPPORTED otherwise); asynchronous. */
 int32_t ghn_window_density(const ghn_index_view *ix, int32_t radius, int32_t samples, float *out_density,
                            void *stream);
+
+/* ---------------------------------------------------------- nested grids
+ * Sub-grids for cells holding more than min_points points (SURVEY Appendix B:
+ * cfg3's cell (0,0,0,0) holds 36M of 50M points).  Three steps, all device
+ * arrays caller-owned:
+ *   1. ghn_subgrid_select: the non-empty cells with > min_points points, in
+ *      cell order, into cells_out (capacity n / (min_points + 1) + 1), and
+ *      their number into *n_out (device int32);
+ *   2. ghn_subgrid_bounds: per selected cell the per-dimension min / max of
+ *      its points' coordinates (bmin / bmax, n_sub * d doubles each);
+ *   3. the caller chooses each grid's resolution and fills ghn_subgrid
+ *      records (host logic, copied to the device as `subs`), then
+ *      ghn_subgrid_build counts the points per
+ *      sub-cell (sub_off, E_tot + 1 entries, E_tot = sum of the grids'
+ *      sub-cell counts), scans and scatters them into sub_coords (SoA,
+ *      n_subpts = sum of counts) / sub_idx, and marks sub_of_cell.
+ * workspace: ghn_subgrid_workspace_size(E_tot) bytes. */
+int32_t ghn_subgrid_select(const ghn_index_view *ix, int32_t min_points, int32_t *cells_out, int32_t *n_out,
+                           void *stream);
+int32_t ghn_subgrid_bounds(const ghn_index_view *ix, const int32_t *cells, int32_t n_sub, double *bmin,
+                           double *bmax, void *stream);
+size_t ghn_subgrid_workspace_size(int64_t e_tot);
+int32_t ghn_subgrid_build(const ghn_index_view *ix, const ghn_subgrid *subs, int32_t n_sub, int64_t e_tot, int32_t *sub_off, void *sub_coords, int32_t *sub_idx,
+                          int64_t n_subpts, int32_t *sub_of_cell, void *workspace, size_t workspace_bytes,
+                          void *stream);
 
 /* Number of kernels this library has launched in this process (evidence for
  * the bench's gpu_launches; monotone, thread-safe). */

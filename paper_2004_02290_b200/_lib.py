@@ -36,6 +36,10 @@ EXPORTS = (
     "ghn_gather_i32",
     "ghn_window_density",
     "ghn_launch_count",
+    "ghn_subgrid_select",
+    "ghn_subgrid_bounds",
+    "ghn_subgrid_workspace_size",
+    "ghn_subgrid_build",
 )
 
 _i64, _i32, _f64, _p, _sz = ctypes.c_int64, ctypes.c_int32, ctypes.c_double, ctypes.c_void_p, ctypes.c_size_t
@@ -73,6 +77,18 @@ class IndexView(ctypes.Structure):
         ("pt_off", _p), ("ne_off", _p), ("labels", _p), ("targets", _p), ("labels_perm", _p),
         ("n_labels", _i32), ("metric", _i32),
         ("density_hint", _f64),
+        ("n_sub", _i32), ("sub_min", _i32),
+        ("sub_of_cell", _p), ("subs", _p), ("sub_off", _p), ("sub_coords", _p), ("sub_idx", _p),
+        ("n_subpts", _i64),
+    ]
+
+
+class SubGrid(ctypes.Structure):
+    """ghn_subgrid (include/ghn.h): nested grid of one overfull cell."""
+    _fields_ = [
+        ("origin", _f64 * GHN_MAX_DIM), ("h", _f64 * GHN_MAX_DIM), ("inv_h", _f64 * GHN_MAX_DIM),
+        ("ext", _i32 * GHN_MAX_DIM), ("off", _i64), ("cell", _i32), ("start", _i32), ("count", _i32),
+        ("pad", _i32),
     ]
 
 
@@ -123,6 +139,14 @@ def lib():
     L.ghn_gather_i32.restype = _i32
     L.ghn_window_density.argtypes = [_p, _i32, _i32, _p, _p]
     L.ghn_window_density.restype = _i32
+    L.ghn_subgrid_select.argtypes = [ctypes.POINTER(IndexView), _i32, _p, _p, _p]
+    L.ghn_subgrid_select.restype = _i32
+    L.ghn_subgrid_bounds.argtypes = [ctypes.POINTER(IndexView), _p, _i32, _p, _p, _p]
+    L.ghn_subgrid_bounds.restype = _i32
+    L.ghn_subgrid_workspace_size.argtypes = [_i64]
+    L.ghn_subgrid_workspace_size.restype = _sz
+    L.ghn_subgrid_build.argtypes = [ctypes.POINTER(IndexView), _p, _i32, _i64, _p, _p, _p, _i64, _p, _p, _sz, _p]
+    L.ghn_subgrid_build.restype = _i32
     _lib = L
     return L
 

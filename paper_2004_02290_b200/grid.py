@@ -157,6 +157,7 @@ class GridIndex:
         self.ne_off = t.get("ne_off")
         self.labels_perm = t.get("labels_perm")
         self.n_cells = int(n_cells)
+        self._subgrids = None
         self.lo = np.array(plan.lo[: plan.d], dtype=np.int64)
         self.ext = np.array(plan.ext[: plan.d], dtype=np.int64)
         self._cache: dict = {}
@@ -251,7 +252,18 @@ class GridIndex:
         v.n_labels = self._labels.n_codes
         v.metric = _lib.GHN_METRIC[self.metric]
         v.density_hint = self.density_hint(v)
+        sg = self._subgrids
+        if sg is not None:
+            v.n_sub, v.sub_min = sg["n_sub"], sg["min_points"]
+            v.sub_of_cell, v.subs = _lib.ptr(sg["sub_of_cell"]), _lib.ptr(sg["subs"])
+            v.sub_off, v.sub_coords, v.sub_idx = _lib.ptr(sg["sub_off"]), _lib.ptr(sg["coords"]), _lib.ptr(sg["idx"])
+            v.n_subpts = sg["n_points"]
         return v
+
+    @property
+    def n_subgrids(self) -> int:
+        """Overfull cells carrying a nested grid (0 for most data)."""
+        return 0 if self._subgrids is None else self._subgrids["n_sub"]
 
     def density_hint(self, v=None) -> float:
         """Points per cell the tiled predict sizes its tiles for (2-D DENSE):
@@ -400,7 +412,94 @@ def build_arrays(X, y=None, params: GridParams | None = None, cells_per_axis=Non
                                plan.workspace_bytes, s), "ghn_fit_build")
     n_cells = int(t["n_cells"].item())
     del ws
-    return GridIndex(params, metric, Xd, labels, plan, t, n_cells)
+    index = GridIndex(params, metric, Xd, labels, plan, t, n_cells)
+    _build_subgrids(index)
+    return index
+
+
+# Cells holding more than SUBGRID_MIN_POINTS points get a nested grid of about
+# SUBGRID_POINTS_PER_CELL points per sub-cell (csrc/ghn_subgrid.cu; cfg3's
+# cell (0,0,0,0) holds 36M points).  Pure acceleration: results are unchanged.
+SUBGRID_MIN_POINTS = 1024
+SUBGRID_POINTS_PER_CELL = 8
+
+
+def subgrid_resolution(bmin, bmax, count, points_per_cell=SUBGRID_POINTS_PER_CELL):
+    """Sub-cells per dimension for a cell's bounding box: about
+    count / points_per_cell cubes of a common side, one split along
+    dimensions of zero extent (host logic)."""
+    ext = np.asarray(bmax, dtype=np.float64) - np.asarray(bmin, dtype=np.float64)
+    d = ext.shape[0]
+    pos = ext > 0
+    if not pos.any():
+        return np.ones(d, dtype=np.int64)
+    m = max(1, int(count) // points_per_cell)
+    h = float(np.exp(np.log(ext[pos]).sum() / pos.sum() - np.log(m) / pos.sum()))
+    for _ in range(200):
+        s = np.where(pos, np.clip(np.ceil(ext / h), 1, 1 << 16), 1).astype(np.int64)
+        if float(np.prod(s, dtype=np.float64)) <= 2 * m + 16:
+            return s
+        h *= 1.1
+    return s
+
+
+def _build_subgrids(index: GridIndex, min_points: int = SUBGRID_MIN_POINTS) -> None:
+    import torch
+
+    L = _lib.lib()
+    n, d = index.size, index.dim
+    if index.n_cells == 0 or n <= min_points:
+        return
+    dev = index.X.device
+    s = _lib.stream_handle()
+    v = index.view()
+    cap = n // (min_points + 1) + 1
+    cells = torch.empty(cap, dtype=torch.int32, device=dev)
+    cnt = torch.zeros(1, dtype=torch.int32, device=dev)
+    _lib.check(L.ghn_subgrid_select(ctypes.byref(v), min_points, _lib.ptr(cells), _lib.ptr(cnt), s),
+               "ghn_subgrid_select")
+    n_sub = int(cnt.item())
+    if n_sub == 0:
+        return
+    cells = torch.sort(cells[:n_sub])[0].contiguous()
+    bmin = torch.empty((n_sub, d), dtype=torch.float64, device=dev)
+    bmax = torch.empty((n_sub, d), dtype=torch.float64, device=dev)
+    _lib.check(L.ghn_subgrid_bounds(ctypes.byref(v), _lib.ptr(cells), n_sub, _lib.ptr(bmin), _lib.ptr(bmax), s),
+               "ghn_subgrid_bounds")
+    cells_h = cells.cpu().numpy()
+    starts = index.cell_start[cells.long()].cpu().numpy()
+    ends = index.cell_start[cells.long() + 1].cpu().numpy()
+    bmin_h, bmax_h = bmin.cpu().numpy(), bmax.cpu().numpy()
+    recs = (_lib.SubGrid * n_sub)()
+    off = 0
+    for g in range(n_sub):
+        cnt_g = int(ends[g] - starts[g])
+        ext = subgrid_resolution(bmin_h[g], bmax_h[g], cnt_g)
+        r = recs[g]
+        for j in range(d):
+            span = float(bmax_h[g, j] - bmin_h[g, j])
+            h = span / float(ext[j]) if span > 0 else 1.0
+            r.origin[j] = float(bmin_h[g, j])
+            r.h[j] = h
+            r.inv_h[j] = 1.0 / h
+            r.ext[j] = int(ext[j])
+        r.off, r.cell, r.start, r.count = off, int(cells_h[g]), int(starts[g]), cnt_g
+        off += int(np.prod(ext))
+    e_tot = off
+    n_points = int((ends - starts).sum())
+    subs = torch.frombuffer(bytearray(bytes(recs)), dtype=torch.uint8).to(dev)
+    sub_off = torch.empty(e_tot + 1, dtype=torch.int32, device=dev)
+    coords = torch.empty(d * n_points, dtype=index.coords_soa.dtype, device=dev)
+    idx = torch.empty(n_points, dtype=torch.int32, device=dev)
+    sub_of_cell = torch.empty(index.n_cells, dtype=torch.int32, device=dev)
+    wsz = int(L.ghn_subgrid_workspace_size(e_tot))
+    ws = torch.empty(wsz, dtype=torch.uint8, device=dev)
+    _lib.check(L.ghn_subgrid_build(ctypes.byref(v), _lib.ptr(subs), n_sub, e_tot, _lib.ptr(sub_off),
+                                   _lib.ptr(coords), _lib.ptr(idx), n_points, _lib.ptr(sub_of_cell),
+                                   _lib.ptr(ws), wsz, s), "ghn_subgrid_build")
+    index._subgrids = {"n_sub": n_sub, "min_points": min_points, "sub_of_cell": sub_of_cell, "subs": subs,
+                       "sub_off": sub_off, "coords": coords, "idx": idx, "n_points": n_points,
+                       "records": recs}
 
 
 def cell_points(index: GridIndex, cell) -> list[int]:

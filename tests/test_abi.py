@@ -66,5 +66,33 @@ def test_struct_layouts_match_header():
     assert ctypes.sizeof(_lib.QueryOut) == 7 * 8
     assert _lib.IndexView.coords.offset == 8 + 4 * 4 + 8 + 16 * 8 + 8 + 16 * 8 * 2
     assert _lib.IndexView.density_hint.offset == 8 + 4 * 4 + 8 + 16 * 8 + 8 + 16 * 8 * 2 + 9 * 8 + 2 * 4
-    assert ctypes.sizeof(_lib.IndexView) == 512
+    assert _lib.IndexView.n_sub.offset == 512
+    assert ctypes.sizeof(_lib.IndexView) == 512 + 8 + 5 * 8 + 8
+    assert ctypes.sizeof(_lib.SubGrid) == 16 * 8 * 3 + 16 * 4 + 8 + 4 * 4
     assert ctypes.sizeof(_lib.FitPlan) == 8 + 4 * 4 + 8 + 16 * 8 * 3 + 8 * 3
+
+
+@pytest.mark.skipif(__import__("shutil").which("gcc") is None, reason="gcc not available")
+def test_struct_layouts_match_compiled_header(tmp_path):
+    """offsetof / sizeof of every ABI struct, compiled from include/ghn.h,
+    equal the ctypes mirror in _lib.py."""
+    import subprocess
+
+    structs = {"ghn_fit_plan": _lib.FitPlan, "ghn_fit_out": _lib.FitOut, "ghn_index_view": _lib.IndexView,
+               "ghn_query_out": _lib.QueryOut, "ghn_subgrid": _lib.SubGrid}
+    lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "ghn.h"', "int main(void) {"]
+    for cname, py in structs.items():
+        lines.append(f'printf("{cname} size %zu\\n", sizeof({cname}));')
+        for fname, _ in py._fields_:
+            lines.append(f'printf("{cname} {fname} %zu\\n", offsetof({cname}, {fname}));')
+    lines.append("return 0; }")
+    src = tmp_path / "layout.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "layout"
+    subprocess.run(["gcc", "-I", os.path.dirname(HEADER), str(src), "-o", str(exe)], check=True)
+    out = subprocess.run([str(exe)], check=True, capture_output=True, text=True).stdout.split("\n")
+    for line in filter(None, out):
+        cname, field, val = line.split()
+        py = structs[cname]
+        got = ctypes.sizeof(py) if field == "size" else getattr(py, field).offset
+        assert got == int(val), (cname, field, got, val)
