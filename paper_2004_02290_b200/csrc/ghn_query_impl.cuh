@@ -235,40 +235,6 @@ __device__ __forceinline__ double escape_key(double gap, int metric) {
     return metric == GHN_METRIC_EUCLIDEAN ? __dmul_rn(gap, gap) : gap;
 }
 
-// Lower bound over the cells of dimension jl in [c0, c1] given the other
-// dimensions' gaps: trims the interval to the cells whose bound can be <= thr
-// (the bound is non-increasing up to the query's cell `qc` and non-decreasing
-// after it).  Returns false when no cell survives.
-template <int D, typename GapFn>
-__device__ __forceinline__ bool trim_interval(double *gap, int d, int jl, int metric, double thr, int64_t qc,
-                                              int64_t &c0, int64_t &c1, GapFn gap_at) {
-    auto ok = [&](int64_t c) {
-        gap[jl] = gap_at(c);
-        return gap_key<D>(gap, d, metric) <= thr;
-    };
-    const int64_t m = qc < c0 ? c0 : (qc > c1 ? c1 : qc);
-    if (!ok(m)) return false;
-    if (!ok(c0)) {   // first ok cell in (c0, m]
-        int64_t lo = c0, hi = m;
-        while (hi - lo > 1) {
-            const int64_t mid = lo + (hi - lo) / 2;
-            if (ok(mid)) hi = mid;
-            else lo = mid;
-        }
-        c0 = hi;
-    }
-    if (!ok(c1)) {   // last ok cell in [m, c1)
-        int64_t lo = m, hi = c1;
-        while (hi - lo > 1) {
-            const int64_t mid = lo + (hi - lo) / 2;
-            if (ok(mid)) lo = mid;
-            else hi = mid;
-        }
-        c1 = lo;
-    }
-    return true;
-}
-
 // ------------------------------------------------------------ sub-grid walk
 // Nearest members of one overfull cell (its nested grid, ghn_subgrid.cu):
 // rings of sub-cells around the query's (clamped) sub-cell, each sub-cell
@@ -277,7 +243,7 @@ __device__ __forceinline__ bool trim_interval(double *gap, int d, int jl, int me
 // Every member that can enter the top-k is evaluated, so the top-k after the
 // walk equals the top-k after scanning the whole cell (explore.py:110-118).
 template <typename T, int D, int KS>
-__device__ __noinline__ void sub_walk(const QArgs &a, const double *qd, int d, int32_t gid, TopK<KS> &tk, bool &changed) {
+__device__ __forceinline__ void sub_walk(const QArgs &a, const double *qd, int d, int32_t gid, TopK<KS> &tk, bool &changed) {
     constexpr int DM = D > 0 ? D : GHN_MAX_DIM;
     const int lane = lane_id();
     const ghn_subgrid &g = a.ix.subs[gid];
@@ -301,7 +267,8 @@ __device__ __noinline__ void sub_walk(const QArgs &a, const double *qd, int d, i
         if (r > 0 && tk.filled >= k) {
             // every unvisited sub-cell lies outside block(r-1) in some dimension
             double esc = INFINITY;
-            for (int j = 0; j < d; ++j) {
+            _Pragma("unroll") for (int j = 0; j < DM; ++j) {
+                if (j >= d) break;
                 if (c[j] - (r - 1) > 0) {
                     const double face = widen_hi(g.origin[j] + (double)(c[j] - r + 1) * g.h[j], g.h[j]);
                     esc = fmin(esc, __dsub_rn(qd[j], face));
@@ -315,7 +282,8 @@ __device__ __noinline__ void sub_walk(const QArgs &a, const double *qd, int d, i
         }
         int32_t lo_c[DM], hi_c[DM];
         int64_t rows = 1;
-        for (int j = 0; j < d; ++j) {
+        _Pragma("unroll") for (int j = 0; j < DM; ++j) {
+                if (j >= d) break;
             lo_c[j] = (int32_t)max((int64_t)0, (int64_t)c[j] - r);
             hi_c[j] = (int32_t)min((int64_t)ext[j] - 1, (int64_t)c[j] + r);
             if (j < jl) rows *= hi_c[j] - lo_c[j] + 1;
@@ -327,7 +295,8 @@ __device__ __noinline__ void sub_walk(const QArgs &a, const double *qd, int d, i
                 double gap[DM];
                 uint32_t rem = (uint32_t)t;
                 int64_t cheb = 0, rowlin = 0, mul = 1;
-                for (int j = jl - 1; j >= 0; --j) {
+                _Pragma("unroll") for (int j = DM - 2; j >= 0; --j) {
+                    if (j >= jl) continue;
                     const uint32_t len = (uint32_t)(hi_c[j] - lo_c[j] + 1);
                     const uint32_t q = rem / len;
                     const int64_t rj = lo_c[j] + (int64_t)(rem - q * len);
@@ -339,24 +308,24 @@ __device__ __noinline__ void sub_walk(const QArgs &a, const double *qd, int d, i
                 }
                 const int64_t base = g.off + rowlin * ext[jl];
                 const bool full = tk.filled >= k;
-                auto gap_at = [&](int64_t z) { return sub_gap(g, jl, qd[jl], z, z); };
                 if (cheb == r) {
-                    int64_t z0 = lo_c[jl], z1 = hi_c[jl];
-                    if (!full || trim_interval<D>(gap, d, jl, metric, tk.thr_key, c[jl], z0, z1, gap_at)) {
+                    const int64_t z0 = lo_c[jl], z1 = hi_c[jl];
+                    gap[jl] = sub_gap(g, jl, qd[jl], z0, z1);
+                    if (!full || gap_key<D>(gap, d, metric) <= tk.thr_key) {
                         s0 = a.ix.sub_off[base + z0];
                         n0 = a.ix.sub_off[base + z1 + 1] - s0;
                     }
                 } else {
                     const int64_t za = (int64_t)c[jl] - r, zb = (int64_t)c[jl] + r;
                     if (za >= 0) {
-                        gap[jl] = gap_at(za);
+                        gap[jl] = sub_gap(g, jl, qd[jl], za, za);
                         if (!full || gap_key<D>(gap, d, metric) <= tk.thr_key) {
                             s0 = a.ix.sub_off[base + za];
                             n0 = a.ix.sub_off[base + za + 1] - s0;
                         }
                     }
                     if (zb < ext[jl] && zb != za) {
-                        gap[jl] = gap_at(zb);
+                        gap[jl] = sub_gap(g, jl, qd[jl], zb, zb);
                         if (!full || gap_key<D>(gap, d, metric) <= tk.thr_key) {
                             s1 = a.ix.sub_off[base + zb];
                             n1 = a.ix.sub_off[base + zb + 1] - s1;
@@ -384,8 +353,10 @@ __device__ __forceinline__ void drain_fat(const QArgs &a, const double *qd, int 
 }
 
 // Visit the non-empty cells at Chebyshev distance exactly l.  Returns the
-// next non-empty layer when it is known (cell-list scan), else l + 1.
-template <typename T, int D, int KS>
+// next non-empty layer when it is known (cell-list scan), else l + 1.  SUB:
+// the index has nested grids (overfull cells are walked by sub-cell rings);
+// the other instantiation carries none of that code.
+template <typename T, int D, int KS, bool SUB>
 __device__ __forceinline__ int64_t visit_layer(const QArgs &a, const double *qd, const int64_t *r, int d, int64_t l,
                                                bool want_stats, TopK<KS> &tk, LayerAcc &acc) {
     constexpr int DM = D > 0 ? D : GHN_MAX_DIM;
@@ -415,7 +386,8 @@ __device__ __forceinline__ int64_t visit_layer(const QArgs &a, const double *qd,
         // in some dimension; if that escape distance already exceeds the
         // k-th key, no point of the shell can enter (changed stays false)
         double esc = INFINITY;
-        for (int j = 0; j < d; ++j) {
+        _Pragma("unroll") for (int j = 0; j < DM; ++j) {
+                if (j >= d) break;
             const double w = ix.widths[j];
             if (r[j] - (l - 1) > 0)
                 esc = fmin(esc, __dsub_rn(qd[j], widen_hi(__dmul_rn((double)(ix.lo[j] + r[j] - l + 1), w), w)));
@@ -424,7 +396,7 @@ __device__ __forceinline__ int64_t visit_layer(const QArgs &a, const double *qd,
         }
         if (esc != INFINITY && escape_key(esc, metric) > tk.thr_key) return l + 1;
     }
-    const bool subs = ix.n_sub > 0;
+    constexpr bool subs = SUB;
     if (ix.layout == GHN_LAYOUT_LIST || rows > (double)ix.n_cells) {
         // cell-list scan (explore.py:105), also finds the next non-empty layer
         int64_t next = INT64_MAX;
@@ -434,7 +406,8 @@ __device__ __forceinline__ int64_t visit_layer(const QArgs &a, const double *qd,
             int32_t st = 0, cntp = 0, gid = -1;
             if (c < ix.n_cells) {
                 int64_t ch = 0;
-                for (int j = 0; j < d; ++j) {
+                _Pragma("unroll") for (int j = 0; j < DM; ++j) {
+                if (j >= d) break;
                     int64_t v = iabs64((int64_t)ix.cell_ids[(int64_t)c * d + j] - r[j]);
                     ch = v > ch ? v : ch;
                 }
@@ -449,13 +422,14 @@ __device__ __forceinline__ int64_t visit_layer(const QArgs &a, const double *qd,
             acc.points += warp_sum(cntp);
             if (match && tk.filled >= k) {
                 double gap[DM];
-                for (int j = 0; j < d; ++j) {
+                _Pragma("unroll") for (int j = 0; j < DM; ++j) {
+                if (j >= d) break;
                     const int64_t id = ix.cell_ids[(int64_t)c * d + j];
                     gap[j] = cell_gap(ix, j, qd[j], id, id);
                 }
                 if (gap_key<D>(gap, d, metric) > tk.thr_key) cntp = 0;
             }
-            if (subs && cntp > ix.sub_min) {
+            if (SUB && cntp > ix.sub_min) {
                 gid = ix.sub_of_cell[c];
                 if (gid >= 0) {
                     fat = true;
@@ -463,7 +437,7 @@ __device__ __forceinline__ int64_t visit_layer(const QArgs &a, const double *qd,
                 }
             }
             if (__any_sync(GHN_FULL, cntp > 0)) consume<T, D, KS>(a, main_src, qd, d, st, cntp, 0, 0, tk, acc.changed);
-            if (subs) drain_fat<T, D, KS>(a, qd, d, fat, gid, tk, acc.changed);
+            if (SUB) drain_fat<T, D, KS>(a, qd, d, fat, gid, tk, acc.changed);
         }
         return warp_min(next);
     }
@@ -486,7 +460,8 @@ __device__ __forceinline__ int64_t visit_layer(const QArgs &a, const double *qd,
             uint32_t rem = (uint32_t)t;
             int64_t cheb = 0;
             uint32_t rowlin = 0, mul = 1;
-            for (int j = jl - 1; j >= 0; --j) {
+            _Pragma("unroll") for (int j = DM - 2; j >= 0; --j) {
+                    if (j >= jl) continue;
                 const uint32_t len = (uint32_t)(hi_c[j] - lo_c[j] + 1);
                 uint32_t q = rem, rj = (uint32_t)lo_c[j];
                 if (len != 1) {
@@ -526,42 +501,42 @@ __device__ __forceinline__ int64_t visit_layer(const QArgs &a, const double *qd,
         acc.cells += warp_sum(cells);
         acc.points += warp_sum(n0 + n1);
         if (t < R && tk.filled >= k && n0 + n1 > 0) {
+            // whole-row / per-end-cell lower bounds against the k-th key
             double gap[DM];
-            for (int j = 0; j < jl; ++j) gap[j] = cell_gap(ix, j, qd[j], rid[j], rid[j]);
-            auto gap_at = [&](int64_t z) { return cell_gap(ix, jl, qd[jl], z, z); };
+#pragma unroll
+            for (int j = 0; j < DM; ++j)
+                if (j < jl) gap[j] = cell_gap(ix, j, qd[j], rid[j], rid[j]);
             if (x0 <= x1) {
-                if (trim_interval<D>(gap, d, jl, metric, tk.thr_key, r[jl], x0, x1, gap_at)) {
-                    s0 = ix.pt_off[rowbase + x0];
-                    n0 = ix.pt_off[rowbase + x1 + 1] - s0;
-                } else {
+                gap[jl] = cell_gap(ix, jl, qd[jl], x0, x1);
+                if (gap_key<D>(gap, d, metric) > tk.thr_key) {
                     n0 = 0;
                     x0 = 1, x1 = 0;
                 }
             }
             if (y0 <= y1) {
-                gap[jl] = gap_at(y0);
+                gap[jl] = cell_gap(ix, jl, qd[jl], y0, y1);
                 if (gap_key<D>(gap, d, metric) > tk.thr_key) {
                     n1 = 0;
                     y0 = 1, y1 = 0;
                 }
             }
         }
-        if (subs && n0 + n1 > ix.sub_min) {   // may hold an overfull cell: cell by cell below
+        if (SUB && n0 + n1 > ix.sub_min) {   // may hold an overfull cell: cell by cell below
             heavy = true;
             n0 = n1 = 0;
         }
         if (__any_sync(GHN_FULL, n0 + n1 > 0)) consume<T, D, KS>(a, main_src, qd, d, s0, n0, s1, n1, tk, acc.changed);
-        if (!subs) continue;
+        if (!SUB) continue;
         unsigned hm = __ballot_sync(GHN_FULL, heavy);
         while (hm) {
             const int src = __ffs(hm) - 1;
             hm &= hm - 1;
             int32_t brid[DM];
-            for (int j = 0; j < jl; ++j) brid[j] = __shfl_sync(GHN_FULL, rid[j], src);
+            _Pragma("unroll") for (int j = 0; j < DM; ++j) if (j < jl) brid[j] = __shfl_sync(GHN_FULL, rid[j], src);
             const int64_t bbase = __shfl_sync(GHN_FULL, rowbase, src);
             const int64_t iv[4] = {__shfl_sync(GHN_FULL, x0, src), __shfl_sync(GHN_FULL, x1, src),
                                    __shfl_sync(GHN_FULL, y0, src), __shfl_sync(GHN_FULL, y1, src)};
-            for (int h = 0; h < 2; ++h) {
+            _Pragma("unroll") for (int h = 0; h < 2; ++h) {
                 for (int64_t zb = iv[2 * h]; zb <= iv[2 * h + 1]; zb += 32) {
                     const int64_t z = zb + lane;
                     int32_t st = 0, cnt = 0, gid = -1;
@@ -571,7 +546,7 @@ __device__ __forceinline__ int64_t visit_layer(const QArgs &a, const double *qd,
                         cnt = ix.pt_off[bbase + z + 1] - st;
                         if (cnt > 0 && tk.filled >= k) {
                             double gap[DM];
-                            for (int j = 0; j < jl; ++j) gap[j] = cell_gap(ix, j, qd[j], brid[j], brid[j]);
+                            _Pragma("unroll") for (int j = 0; j < DM; ++j) if (j < jl) gap[j] = cell_gap(ix, j, qd[j], brid[j], brid[j]);
                             gap[jl] = cell_gap(ix, jl, qd[jl], z, z);
                             if (gap_key<D>(gap, d, metric) > tk.thr_key) cnt = 0;
                         }
@@ -639,7 +614,7 @@ __device__ double pairwise_mean(const double (&v)[KS], int k) {
     return __ddiv_rn(s, (double)k);
 }
 
-template <typename T, int D, int KS>
+template <typename T, int D, int KS, bool SUB>
 __device__ __forceinline__ void query_one(const QArgs &a, int64_t w) {
     constexpr int DM = D > 0 ? D : GHN_MAX_DIM;
     const int lane = lane_id();
@@ -681,7 +656,7 @@ __device__ __forceinline__ void query_one(const QArgs &a, int64_t w) {
     }
     for (; a.mode != GHN_MODE_BRUTE;) {
         LayerAcc acc{false, 0, 0};
-        const int64_t next = visit_layer<T, D, KS>(a, qd, r, d, l, want_stats, tk, acc);
+        const int64_t next = visit_layer<T, D, KS, SUB>(a, qd, r, d, l, want_stats, tk, acc);
         cells += acc.cells;
         points += acc.points;
         layers = l;
@@ -869,27 +844,27 @@ __device__ __forceinline__ void query_one(const QArgs &a, int64_t w) {
     }
 }
 
-template <typename T, int D, int KS>
+template <typename T, int D, int KS, bool SUB>
 __global__ void __launch_bounds__(Q_THREADS, KS <= 2 ? 4 : (KS == 4 ? 3 : 2)) query_kernel(const QArgs a) {
     const int64_t nqv = a.nq_dev ? (int64_t)*a.nq_dev : a.nq;
     for (int64_t w = (int64_t)blockIdx.x * Q_WARPS + (threadIdx.x >> 5); w < nqv;
          w += (int64_t)gridDim.x * Q_WARPS)
-        query_one<T, D, KS>(a, w);
+        query_one<T, D, KS, SUB>(a, w);
 }
 
 // ------------------------------------------------------------ launch
-template <typename T, int D>
+template <typename T, int D, bool SUB>
 int32_t launch_query_d(const QArgs &a, int ks, cudaStream_t s) {
     int64_t g = a.nq_dev ? (int64_t)sm_count() * 8 : (a.nq + Q_WARPS - 1) / Q_WARPS;
     if (g > 0x7fffffffLL) g = 0x7fffffffLL;
     const unsigned grid = (unsigned)g;
     switch (ks) {
-        case 1: query_kernel<T, D, 1><<<grid, Q_THREADS, 0, s>>>(a); break;
-        case 2: query_kernel<T, D, 2><<<grid, Q_THREADS, 0, s>>>(a); break;
-        case 4: query_kernel<T, D, 4><<<grid, Q_THREADS, 0, s>>>(a); break;
+        case 1: query_kernel<T, D, 1, SUB><<<grid, Q_THREADS, 0, s>>>(a); break;
+        case 2: query_kernel<T, D, 2, SUB><<<grid, Q_THREADS, 0, s>>>(a); break;
+        case 4: query_kernel<T, D, 4, SUB><<<grid, Q_THREADS, 0, s>>>(a); break;
         default:
             // k > 128: runtime-d only
-            query_kernel<T, 0, 8><<<grid, Q_THREADS, 0, s>>>(a);
+            query_kernel<T, 0, 8, SUB><<<grid, Q_THREADS, 0, s>>>(a);
             break;
     }
     GHN_LAUNCH_CHECK("query_kernel");
@@ -898,19 +873,24 @@ int32_t launch_query_d(const QArgs &a, int ks, cudaStream_t s) {
 
 // Kernels are specialised for the dimensions the configs use (2, 3, 4, 6) on
 // fp32 indexes; everything else (fp64 indexes, other d) runs the runtime-d
-// instantiation -- same arithmetic, loops not unrolled.
+// instantiation -- same arithmetic, loops not unrolled.  Indexes with nested
+// grids run the SUB instantiation (d = 4 specialised: cfg3).
 template <typename T>
 int32_t launch_query(const QArgs &a, int ks, cudaStream_t s) {
+    if (a.ix.n_sub > 0) {
+        if (sizeof(T) == 4 && a.ix.d == 4) return launch_query_d<T, 4, true>(a, ks, s);
+        return launch_query_d<T, 0, true>(a, ks, s);
+    }
     if (sizeof(T) == 4) {
         switch (a.ix.d) {
-            case 2: return launch_query_d<T, 2>(a, ks, s);
-            case 3: return launch_query_d<T, 3>(a, ks, s);
-            case 4: return launch_query_d<T, 4>(a, ks, s);
-            case 6: return launch_query_d<T, 6>(a, ks, s);
+            case 2: return launch_query_d<T, 2, false>(a, ks, s);
+            case 3: return launch_query_d<T, 3, false>(a, ks, s);
+            case 4: return launch_query_d<T, 4, false>(a, ks, s);
+            case 6: return launch_query_d<T, 6, false>(a, ks, s);
             default: break;
         }
     }
-    return launch_query_d<T, 0>(a, ks, s);
+    return launch_query_d<T, 0, false>(a, ks, s);
 }
 
 }  // namespace
