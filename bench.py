@@ -1,6 +1,7 @@
 #!/usr/bin/env python
 """GHN bench: BASELINE.json's metric on config 4 (2-D, 100M points, 10M
-queries, C=4096, k sweep {1,4,16,64}, majority vote) on 1..N B200s.
+queries, C=4096, k sweep {1,4,16,64}, majority vote) on 1..N B200s, plus
+one measurement block per other config (cfg0-3, `configs`).
 
 One step = one batched predict of all nq queries for every k of the sweep
 (4 x nq queries), inputs resident in HBM.  Per k: query binning
@@ -15,9 +16,17 @@ exceed L2 (126 MB) and L2 is also flushed between steps.
             next k's predict)
   roofline  predict kernel: algorithmic bytes (4d(1+S_q) + 4
             per query, S_q = points scanned) / kernel time vs measured HBM peak
-  fit       grid build (fit) points/s, device-resident input
+  fit       grid build (fit) points/s, device-resident input, with its HBM
+            roofline (B_fit = n(8d+8) + 4(E+1)) and the
+            reference's array-path build (grid.py:184-195) timed on this host
+  parity_checked  after timing, a seeded sample of the TIMED outputs (labels
+            and confidences / means) compared with the C oracle, bit-exact
+  configs   cfg0-3: the same measurement per config (queries/s, fit, a
+            roofline -- HBM for cfg0/1, the FP64 pipe for cfg2/3 whose
+            pruned predict evaluates far fewer candidates than the
+            reference scans -- and parity_checked)
   cpu_baseline  the oracle port (numpy restatement of the reference
-            algorithm) on a bounded query sample on this host
+            algorithm) on a bounded query sample on this host's cores
 
 Multi-GPU (--gpus N under torchrun): replicas -- every rank builds the same
 index and predicts its own 10M-query shard (weak scaling, no data-path
@@ -54,7 +63,11 @@ def parse_args(argv=None):
     ap.add_argument("--ks", type=str, default=None, help="k sweep, default: the config's")
     ap.add_argument("--n", type=int, default=None, help="override n_train (debug only)")
     ap.add_argument("--nq", type=int, default=None, help="override queries per rank (debug only)")
-    ap.add_argument("--cpu-sample", type=int, default=4, help="port queries per k for cpu_baseline (~10 s)")
+    ap.add_argument("--cpu-sample", type=int, default=100, help="port queries per k for cpu_baseline")
+    ap.add_argument("--configs", type=str, default="0,1,2,3",
+                    help="other configs measured in the same run ('' = none)")
+    ap.add_argument("--config-steps", type=int, default=3)
+    ap.add_argument("--parity-sample", type=int, default=20000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     return ap.parse_args(argv)
@@ -302,11 +315,190 @@ def run_reference(args):
     return 0
 
 
+def fp_peaks():
+    """FP64 / FP32 add+mul issue peaks of this GPU, from the committed
+    micro-benchmark (tools/micro/fppeak.cu -> profiles/fp_peaks.json)."""
+    try:
+        with open(os.path.join(REPO, "profiles", "fp_peaks.json")) as fh:
+            return json.load(fh)
+    except Exception:
+        return None
+
+
+def fit_algorithmic_bytes(n, d, E):
+    """read the coordinates, write them permuted, the
+    permutation and the permuted labels (n(8d+8)), plus the offsets table."""
+    return n * (8 * d + 8) + 4 * (E + 1)
+
+
+def time_fit(build, flush, stream, reps=2):
+    """Fit time (ms, best of reps) with L2 flushed before each build."""
+    import torch
+
+    index = build()
+    best = None
+    for _ in range(reps):
+        flush.zero_()
+        del index
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        index = build()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        t = e0.elapsed_time(e1)
+        best = t if best is None else min(best, t)
+    return index, best
+
+
+def parity_check(w, k, out, ref, sample, seed):
+    """Seeded sample of the TIMED predict outputs against the C oracle
+    (bit-exact: labels + confidences, or means)."""
+    import numpy as np
+
+    import oracle
+
+    rng = np.random.default_rng(seed)
+    nq = w.Q.shape[0]
+    sel = np.sort(rng.choice(nq, size=min(sample, nq), replace=False))
+    keys, idx, _ = ref.query(w.Q[sel], k, "heuristic")
+    if w.task == "classify":
+        lab, conf = oracle.classify(keys, idx, np.asarray(w.y, dtype=np.int64))
+        got_l = out["label"].cpu().numpy()[sel].astype(np.int64)
+        got_c = out["confidence"].cpu().numpy()[sel]
+        bad = int(np.count_nonzero((got_l != lab) | (got_c != conf)))
+        what = "labels + confidences"
+    else:
+        val = oracle.regress_mean(idx, np.asarray(w.y, dtype=np.float64))
+        bad = int(np.count_nonzero(out["value"].cpu().numpy()[sel] != val))
+        what = "means"
+    return {"ok": bad == 0, "queries": int(sel.size), "mismatches": bad, "k": k, "checked": what,
+            "against": "oracle/ghn_oracle.c (C restatement pinned to reference fixtures)"}
+
+
+def measure(w, ks, flush, stream, steps, warmup, world=1, rank=0, clocks=None, keep_outputs=True):
+    """Fit + per-k timed predict of one workload.  A step = one predict_batch
+    of all queries per k (binning, kernels, fallbacks) with the confidence
+    output, on the launching stream, L2 flushed before every step."""
+    import numpy as np
+    import torch
+
+    from paper_2004_02290_b200 import _lib, build_arrays, predict_batch
+
+    L = _lib.lib()
+    dev = torch.device("cuda", torch.cuda.current_device())
+    X_d = torch.from_numpy(w.X).to(dev)
+    y_d = torch.from_numpy(w.y).to(dev)
+    Q_d = torch.from_numpy(w.Q).to(dev)
+    n, d = w.X.shape
+    nq = w.Q.shape[0]
+    index, fit_ms = time_fit(lambda: build_arrays(X_d, y_d, cells_per_axis=w.cells_per_axis), flush, stream)
+    E = int(index.plan.E) if index.layout == "dense" else int(index.n_cells)
+
+    # work counters per k (untimed): reference points_scanned, keys the device evaluated
+    scanned = {}
+    for k in ks:
+        tot = predict_batch(index, Q_d, k, task=w.task, totals=True, confidence=False)["totals"].cpu().numpy()
+        scanned[k] = {"layers": int(tot[0]), "cells": int(tot[1]), "points": int(tot[2]), "keys": int(tot[4])}
+
+    outs = {}
+
+    def step():
+        ev = []
+        for k in ks:
+            e0, e1 = (torch.cuda.Event(enable_timing=True) for _ in range(2))
+            e0.record(stream)
+            r = predict_batch(index, Q_d, k, task=w.task)
+            e1.record(stream)
+            ev.append((k, e0, e1))
+            if keep_outputs:
+                outs[k] = r
+        return ev
+
+    for _ in range(warmup):
+        flush.zero_()
+        step()
+    torch.cuda.synchronize()
+    per_k_ms = {k: 0.0 for k in ks}
+    launches0 = int(L.ghn_launch_count())
+    cm = clocks if clocks is not None else _Null()
+    with cm:
+        for _ in range(steps):
+            flush.zero_()
+            barrier(world)
+            torch.cuda.synchronize()
+            evs = step()
+            torch.cuda.synchronize()
+            barrier(world)
+            for k, e0, e1 in evs:
+                per_k_ms[k] += e0.elapsed_time(e1)
+    launches = int(L.ghn_launch_count()) - launches0
+    per_k_ms = {k: v / steps for k, v in per_k_ms.items()}
+    return {"index": index, "fit_ms": fit_ms, "E": E, "scanned": scanned, "per_k_ms": per_k_ms,
+            "launches": launches, "outs": outs, "n": n, "d": d, "nq": nq, "Q_d": Q_d}
+
+
+class _Null:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        return False
+
+
+def fit_block(m, peak, peak_kind):
+    b = fit_algorithmic_bytes(m["n"], m["d"], m["E"])
+    s = m["fit_ms"] / 1e3
+    return {"points_per_s": m["n"] / s, "ms": m["fit_ms"], "unit": "points/s",
+            "roofline": {"bound": "hbm", "achieved": b / s / 1e9, "peak": peak, "unit": "GB/s",
+                         "frac": b / s / 1e9 / peak, "peak_kind": peak_kind, "algorithmic_bytes": b,
+                         "bytes_formula": "n(8d+8) + 4(E+1) (SURVEY 8(d)), E = cells in the id bounding box"}}
+
+
+CONFIG_TEXT = {
+    0: "2-D uniform, C=32, k=5, vote", 1: "3-D 16-component GMM, C=128, k=10, vote",
+    2: "6-D uniform, C=8, k=16, mean", 3: "4-D lognormal (skewed occupancy), C=64, k=32, vote",
+    4: "2-D uniform, C=4096, k sweep, vote"}
+
+
+def config_block(cfg, w, m, peak, peak_kind, fpp, parity):
+    """One config's measurement: throughput, roofline, fit, parity."""
+    d, nq = m["d"], m["nq"]
+    ks = sorted(m["per_k_ms"])
+    t = sum(m["per_k_ms"].values()) / 1e3
+    qps = len(ks) * nq / t
+    algo = sum(4 * d * (nq + m["scanned"][k]["points"]) + 4 * nq for k in ks)
+    keys = sum(m["scanned"][k]["keys"] for k in ks)
+    out = {"workload": f"cfg{cfg}: {m['n']} x {d}-D, {nq} queries, {CONFIG_TEXT[cfg]}",
+           "queries_per_s": qps, "unit": "queries/s", "predict_ms": {str(k): m["per_k_ms"][k] for k in ks},
+           "mean_points_scanned_ref": {str(k): m["scanned"][k]["points"] / nq for k in ks},
+           "mean_keys_evaluated": {str(k): m["scanned"][k]["keys"] / nq for k in ks},
+           "algorithmic_GBps": algo / t / 1e9,
+           "fit": fit_block(m, peak, peak_kind), "parity_checked": parity}
+    if m["index"].n_subgrids:
+        out["nested_grids"] = m["index"].n_subgrids
+    if cfg in (2, 3) and fpp:
+        ops = keys * (3 * d - 1)     # d subtracts, d squares, d-1 adds per fp64 key (core.py:78-80)
+        fp_peak = fpp["fp64_add_mul_gops"]
+        out["roofline"] = {"bound": "fp64", "achieved": ops / t / 1e9, "peak": fp_peak, "unit": "Gop/s",
+                           "frac": ops / t / 1e9 / fp_peak, "peak_kind": "measured (profiles/fp_peaks.json)",
+                           "ops_formula": "keys evaluated x (3d-1) fp64 add/mul (device work counter)",
+                           "gathered_GBps": keys * 4 * d / t / 1e9,
+                           "why": "pruned predict: the device evaluates mean_keys_evaluated candidates per "
+                                  "query instead of the reference's points_scanned, so the reference-bytes "
+                                  "HBM formula (algorithmic_GBps) exceeds any bandwidth"}
+    else:
+        out["roofline"] = {"bound": "hbm", "achieved": algo / t / 1e9, "peak": peak, "unit": "GB/s",
+                           "frac": algo / t / 1e9 / peak, "peak_kind": peak_kind,
+                           "bytes_formula": "4d(1+S_q)+4 per query, S_q = reference points_scanned"}
+    return out
+
+
 def run_ours(args):
     import numpy as np
     import torch
 
-    from paper_2004_02290_b200 import _lib, build_arrays, datagen, predict_batch
+    from paper_2004_02290_b200 import _lib, datagen, predict_batch
 
     rank, world, local = dist_setup()
     dev = torch.device("cuda", torch.cuda.current_device())
@@ -317,94 +509,34 @@ def run_ours(args):
         rng = np.random.default_rng(1000 + rank)
         w.Q = rng.random(w.Q.shape, dtype=np.float32)
     ks = [int(x) for x in args.ks.split(",")] if args.ks else (list(w.ks) or [w.k])
-    n, d = w.X.shape
-    nq = w.Q.shape[0]
-    L = _lib.lib()
-    X_d = torch.from_numpy(w.X).to(dev)
-    y_d = torch.from_numpy(w.y).to(dev)
-    Q_d = torch.from_numpy(w.Q).to(dev)
     flush = torch.empty(FLUSH_BYTES, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream()
+    peak, peak_kind = peaks()
 
-    # ---- fit (grid build): points/s, device-resident input
-    index = build_arrays(X_d, y_d, cells_per_axis=w.cells_per_axis)
-    fit_ms = []
-    for _ in range(2):
-        flush.zero_()
-        del index
-        torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        index = build_arrays(X_d, y_d, cells_per_axis=w.cells_per_axis)
-        e1.record(stream)
-        torch.cuda.synchronize()
-        fit_ms.append(e0.elapsed_time(e1))
-    fit_s = min(fit_ms) / 1e3
-
-    # ---- algorithmic bytes per k (untimed, deterministic): S_q from the device counters
-    scanned = {}
-    for k in ks:
-        r = predict_batch(index, Q_d, k, task=w.task, totals=True, confidence=False)
-        tot = r["totals"].cpu().numpy()
-        scanned[k] = {"layers": int(tot[0]), "cells": int(tot[1]), "points": int(tot[2])}
-    algo_bytes = {k: 4 * d * (nq + scanned[k]["points"]) + 4 * nq for k in ks}
-
-    def step(timed):
-        # one predict per k: query binning + predict kernel(s) (+ fallbacks)
-        ev = []
-        for k in ks:
-            e0, e1 = (torch.cuda.Event(enable_timing=True) for _ in range(2))
-            e0.record(stream)
-            predict_batch(index, Q_d, k, task=w.task, confidence=False)
-            e1.record(stream)
-            ev.append((k, e0, e1))
-        return ev
-
-    for _ in range(args.warmup):
-        flush.zero_()
-        step(False)
-    torch.cuda.synchronize()
-    per_k_total = {k: 0.0 for k in ks}
-    launches0 = int(L.ghn_launch_count())
-    with ClockSampler(local) as clocks:
-        for _ in range(args.steps):
-            flush.zero_()
-            barrier(world)
-            torch.cuda.synchronize()
-            evs = step(True)
-            torch.cuda.synchronize()
-            barrier(world)
-            for k, e0, e1 in evs:
-                per_k_total[k] += e0.elapsed_time(e1)
-    launches = int(L.ghn_launch_count()) - launches0
-    step_ms = sum(per_k_total.values()) / args.steps
+    clocks = ClockSampler(local)
+    m = measure(w, ks, flush, stream, args.steps, args.warmup, world, rank, clocks=clocks)
+    index, Q_d = m["index"], m["Q_d"]
+    n, d, nq = m["n"], m["d"], m["nq"]
+    step_ms = sum(m["per_k_ms"].values())
     step_ms_max = max_over_ranks(step_ms, world)
     queries_per_step = len(ks) * nq
     value = world * queries_per_step / (step_ms_max / 1e3)
-    kernel_s = sum(per_k_total.values()) / args.steps / 1e3
-    achieved = sum(algo_bytes.values()) / kernel_s / 1e9
-    peak, peak_kind = peaks()
-    per_k = {str(k): {"queries_per_s": nq / (per_k_total[k] / args.steps / 1e3),
-                      "predict_ms": per_k_total[k] / args.steps,
-                      "mean_points_scanned": scanned[k]["points"] / nq,
-                      "mean_layers": scanned[k]["layers"] / nq,
-                      "algo_GBps": algo_bytes[k] / (per_k_total[k] / args.steps / 1e3) / 1e9}
+    algo_bytes = {k: 4 * d * (nq + m["scanned"][k]["points"]) + 4 * nq for k in ks}
+    achieved = sum(algo_bytes.values()) / (step_ms / 1e3) / 1e9
+    per_k = {str(k): {"queries_per_s": nq / (m["per_k_ms"][k] / 1e3),
+                      "predict_ms": m["per_k_ms"][k],
+                      "mean_points_scanned": m["scanned"][k]["points"] / nq,
+                      "mean_layers": m["scanned"][k]["layers"] / nq,
+                      "algo_GBps": algo_bytes[k] / (m["per_k_ms"][k] / 1e3) / 1e9}
              for k in ks}
 
-    # ---- e2e through the public API with host buffers: per step, ONE H2D of
-    # the step's queries (pinned), then the k sweep; each k's labels go back
-    # D2H on a copy stream while the next k computes (copy engines overlap).
+    # ---- e2e through the public API with host buffers (see the module docstring)
     e2e = None
     if not args.no_e2e:
         Q_h = torch.from_numpy(w.Q).pin_memory()
-        out_key = "label" if w.task == "classify" else "value"
-        out_dt = torch.int32 if w.task == "classify" else torch.float64
-        outs_h = [torch.empty(nq, dtype=out_dt).pin_memory() for _ in ks]
-        # Streaming pipeline over the K timed steps: step i+1's queries are
-        # copied H2D (pinned, own stream, double-buffered) while step i
-        # predicts; each k's labels go back D2H on another stream while the
-        # next k computes.  Every step's H2D and D2H are inside the timed
-        # region (the first H2D and the last D2H are not overlapped).
+        keys_out = ("label", "confidence") if w.task == "classify" else ("value",)
+        outs_h = [{o: torch.empty(nq, dtype=torch.int32 if o == "label" else torch.float64).pin_memory()
+                   for o in keys_out} for _ in ks]
         in_stream = torch.cuda.Stream(device=dev)
         out_stream = torch.cuda.Stream(device=dev)
         bufs = [torch.empty_like(Q_d) for _ in range(2)]
@@ -429,14 +561,15 @@ def run_ours(args):
                     issue_h2d(i + 1)
                 stream.wait_event(h2d[b])
                 for j, k in enumerate(ks):
-                    r = predict_batch(index, bufs[b], k, task=w.task, confidence=False)
-                    res = r[out_key]
+                    r = predict_batch(index, bufs[b], k, task=w.task)
                     ev = torch.cuda.Event()
                     ev.record(stream)
                     out_stream.wait_event(ev)
                     with torch.cuda.stream(out_stream):
-                        outs_h[j].copy_(res, non_blocking=True)
-                    res.record_stream(out_stream)
+                        for o in keys_out:
+                            outs_h[j][o].copy_(r[o], non_blocking=True)
+                    for o in keys_out:
+                        r[o].record_stream(out_stream)
                 free[b].record(stream)
             done = torch.cuda.Event()
             done.record(out_stream)
@@ -455,63 +588,100 @@ def run_ours(args):
         e2e_ms = max_over_ranks(e0.elapsed_time(e1) / args.steps, world)
         e2e = {"value": world * queries_per_step / (e2e_ms / 1e3), "unit": "queries/s",
                "h2d_bytes_per_step": int(Q_h.numel() * Q_h.element_size()),
-               "d2h_bytes_per_step": sum(int(o.numel() * o.element_size()) for o in outs_h),
+               "d2h_bytes_per_step": sum(int(t.numel() * t.element_size()) for o in outs_h for t in o.values()),
                "ms_per_step": e2e_ms,
                "pipeline": "K steps back to back: each step's queries H2D from pinned memory on a copy "
                            "stream, double-buffered so step i+1's copy overlaps step i's predicts; each "
-                           "k's labels D2H on a second copy stream overlapping the next k; the first "
-                           "H2D and the last D2H are exposed; no L2 flush (training data 800 MB > L2)"}
+                           "k's labels and confidences D2H on a second copy stream overlapping the next k; "
+                           "the first H2D and the last D2H are exposed; no L2 flush (training data 800 MB > L2)"}
 
-    # ---- CPU legs (rank 0, N=1 only)
-    cpu_baseline = None
-    cpu_c = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        pix, cor = port_index(w)
-        per = max(1, args.cpu_sample)
-        v, cnt = port_queries_per_s(pix, w.Q, ks, per, 1)
-        cpu_baseline = {"value": v, "unit": "queries/s", "cores": 1, "kind": "port",
-                        "sample": f"{per} queries x k in {ks} through oracle/ghn_port.py (reference "
-                                  f"algorithm: O(#cells)={index.n_cells} scan per query and layer) "
-                                  f"+ vote; {cpu_model()}"}
-        th = os.cpu_count() or 1
-        m = min(nq, 200000)
-        t0 = time.perf_counter()
-        for k in ks:
-            keys, idx, _ = cor.query(w.Q[:m], k, threads=th)
-        cpu_c = {"value": len(ks) * m / (time.perf_counter() - t0), "unit": "queries/s", "cores": th,
-                 "sample": f"{m} queries x k in {ks}, oracle/ghn_oracle.c (dense ring enumeration, "
-                           f"OpenMP), neighbours only"}
+    # ---- CPU legs, parity of the timed outputs, other configs (rank 0, N=1 only)
+    cpu_baseline = cpu_c = fit_cpu = parity = None
+    configs = {}
+    if rank == 0 and world == 1:
+        import oracle
+        from oracle import ghn_port
+
+        ref = oracle.COracle(w.X, w.widths)
+        parity = [parity_check(w, k, m["outs"][k], ref, args.parity_sample, 7000 + k) for k in ks]
+        m["outs"].clear()
+        if not args.no_cpu_baseline:
+            order, cids, starts, _, _ = ref.export()
+            pix = ghn_port.PortIndex.from_arrays(w.X, w.y, w.widths, order, starts, cids)
+            procs = os.cpu_count() or 1
+            per = max(1, -(-args.cpu_sample // procs))
+            v, cnt = port_queries_per_s(pix, w.Q, ks, per, procs)
+            cpu_baseline = {"value": v, "unit": "queries/s", "cores": procs, "kind": "port",
+                            "sample": f"{per * procs} queries x k in {ks} through oracle/ghn_port.py (the "
+                                      f"reference algorithm: O(#cells)={index.n_cells} scan per query and "
+                                      f"layer) + vote, forked over {procs} processes; {cpu_model()}; "
+                                      f"numpy {np.__version__}"}
+            m_fit = min(n, 2_000_000)
+            t0 = time.perf_counter()
+            ghn_port.build(w.X[:m_fit], w.y[:m_fit], w.widths)
+            fit_cpu = {"value": m_fit / (time.perf_counter() - t0), "unit": "points/s", "cores": 1,
+                       "kind": "port",
+                       "sample": f"first {m_fit} training points: the reference build's array path "
+                                 f"(floor(x/w) + lexsort + split, grid.py:184-195) in numpy "
+                                 f"{np.__version__}, 1 core (numpy's sort is single-threaded)"}
+            th = os.cpu_count() or 1
+            mq = min(nq, 200000)
+            t0 = time.perf_counter()
+            for k in ks:
+                ref.query(w.Q[:mq], k, threads=th)
+            cpu_c = {"value": len(ks) * mq / (time.perf_counter() - t0), "unit": "queries/s", "cores": th,
+                     "sample": f"{mq} queries x k in {ks}, oracle/ghn_oracle.c (dense ring enumeration, "
+                               f"OpenMP), neighbours only"}
+        del ref
+        fpp = fp_peaks()
+        for c in [int(x) for x in args.configs.split(",") if x.strip()]:
+            if c == cfg:
+                continue
+            wc = datagen.make(c)
+            kc = list(wc.ks) or [wc.k]
+            mc = measure(wc, kc, flush, stream, args.config_steps, 3)
+            refc = oracle.COracle(wc.X, wc.widths)
+            samp = {0: 10000, 3: 300}.get(c, args.parity_sample)
+            par = [parity_check(wc, k, mc["outs"][k], refc, samp, 8000 + c) for k in kc]
+            del refc
+            configs[f"cfg{c}"] = config_block(c, wc, mc, peak, peak_kind, fpp, par)
+            del mc, wc
 
     if rank == 0:
+        fit = fit_block(m, peak, peak_kind)
+        fit["cpu_baseline"] = fit_cpu
         line = {
             "metric": "GHN kNN predict queries/s (k sweep, majority vote)",
             "value": value, "unit": "queries/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": step_ms_max, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"cfg{cfg}: {n} x {d}-D uniform fp32, {nq} queries/rank, "
-                                   f"C={w.cells_per_axis}, k sweep {ks}, heuristic stop, {w.task}",
+                                   f"C={w.cells_per_axis}, k sweep {ks}, heuristic stop, {w.task} "
+                                   f"(label + confidence)",
                        "n_train": n, "queries_per_rank": nq, "k_sweep": ks,
                        "cells_nonempty": index.n_cells, "layout": index.layout,
                        "l2": "flushed between steps (512 MB write); data 800 MB > L2",
                        "storage": "coords fp32 SoA, keys fp64 (numpy einsum order)",
                        "parallelism": f"replicas x{world} (query shards)"},
-            "fit": {"points_per_s": n / fit_s, "ms": fit_s * 1e3, "unit": "points/s"},
+            "fit": fit,
             "per_k": per_k,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "peak_kind": peak_kind,
                          "frac_vs_8000_GBps": achieved / 8000.0,   # the north_star's nominal B200 figure
                          "traffic": ncu_traffic(cfg, ks),
-                         "kernel": "ghn_query: tile2d_thr_kernel, thread per query (+ binning, + query_kernel fallbacks); "
-                                   "time = whole predict call, not the kernel alone",
+                         "kernel": "ghn_query: tile2d_thr_kernel, thread per query (+ binning, + query_kernel "
+                                   "fallbacks); time = whole predict call, not the kernel alone",
                          "algorithmic_bytes_per_step": sum(algo_bytes.values()),
                          "issue_roofline": issue_roofline(),
                          "kernel_stats": ncu_kernel_stats(cfg, ks)},
+            "parity_checked": parity,
             "e2e": e2e,
-            "gpu_launches": launches // args.steps,
-            "gpu_launches_total": launches,
+            "gpu_launches": m["launches"] // args.steps,
+            "gpu_launches_total": m["launches"],
             "clocks": clocks.summary(),
             "cpu_baseline": cpu_baseline,
             "cpu_c_oracle": cpu_c,
+            "configs": configs or None,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -175,7 +175,9 @@ typedef struct ghn_query_out {
     double *confidence;          /* (nq) CLASSIFY: count / k, or NULL */
     double *value;               /* (nq) REGRESS_MEAN / _MEDIAN: the aggregate, or NULL */
     int64_t *stats;              /* (nq, 3) layers_visited, cells_visited, points_scanned, or NULL */
-    unsigned long long *totals;  /* [4] += sum layers, cells, points, queries, or NULL */
+    unsigned long long *totals;  /* [5] += sum layers, cells, points, queries, and candidate keys
+                                    evaluated by the generic kernel (a work counter; the tiled
+                                    kernels leave it), or NULL */
 } ghn_query_out;
 
 /* Workspace for ghn_query / ghn_query_order with nq queries and this k

@@ -41,6 +41,7 @@ struct TopK {
     int filled;          // warp-uniform
     double thr_key;      // k-th entry once filled == k
     int32_t thr_idx;
+    long long nkeys;     // candidate keys evaluated (work counter, totals[4])
 
     __device__ __forceinline__ void init() {
 #pragma unroll
@@ -51,6 +52,7 @@ struct TopK {
         filled = 0;
         thr_key = INFINITY;
         thr_idx = 0x7fffffff;
+        nkeys = 0;
     }
 
     // Insert a warp-uniform candidate known to belong in the top-k.
@@ -131,6 +133,7 @@ __device__ __forceinline__ void consume(const QArgs &a, const Src<T> &src, const
     const int incl = warp_inclusive_scan(cnt);
     const int total = __shfl_sync(GHN_FULL, incl, 31);
     if (total == 0) return;
+    tk.nkeys += total;
     const int excl = incl - cnt;
     const T *__restrict__ coords = src.coords;
     const int64_t n = src.stride;
@@ -727,6 +730,7 @@ __device__ __forceinline__ void query_one(const QArgs &a, int64_t w) {
         atomicAdd(&o.totals[1], (unsigned long long)cells);
         atomicAdd(&o.totals[2], (unsigned long long)points);
         atomicAdd(&o.totals[3], 1ull);
+        atomicAdd(&o.totals[4], (unsigned long long)tk.nkeys);
     }
     if (a.task == GHN_TASK_CLASSIFY && ix.labels) {
         int32_t lab[KS];

@@ -109,7 +109,7 @@ def _run(index: GridIndex, Qt, k, mode, task, want_neighbors, want_stats, want_t
         res["stats"] = torch.empty((nq, 3), dtype=torch.int64, device=dev)
         out.stats = _lib.ptr(res["stats"])
     if want_totals:
-        res["totals"] = torch.zeros(4, dtype=torch.int64, device=dev)
+        res["totals"] = torch.zeros(5, dtype=torch.int64, device=dev)
         out.totals = _lib.ptr(res["totals"])
     if task == _lib.GHN_TASK_CLASSIFY:
         if index._labels.codes is None:

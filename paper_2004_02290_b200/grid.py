@@ -231,7 +231,9 @@ class GridIndex:
         return self._cache["table"]
 
     # -- device view ----------------------------------------------------------
-    def view(self) -> _lib.IndexView:
+    def view(self, density: bool = True) -> _lib.IndexView:
+        """ctypes ghn_index_view of the device tables (density=False skips
+        the tiled predict's density hint, which costs a kernel + sync once)."""
         v = _lib.IndexView()
         p = self.plan
         v.n, v.d, v.dtype, v.layout, v.n_cells, v.E = p.n, p.d, p.dtype, p.layout, self.n_cells, p.E
@@ -251,7 +253,7 @@ class GridIndex:
         v.labels_perm = _lib.ptr(self.labels_perm)
         v.n_labels = self._labels.n_codes
         v.metric = _lib.GHN_METRIC[self.metric]
-        v.density_hint = self.density_hint(v)
+        v.density_hint = self.density_hint(v) if density else 0.0
         sg = self._subgrids
         if sg is not None:
             v.n_sub, v.sub_min = sg["n_sub"], sg["min_points"]
@@ -452,7 +454,7 @@ def _build_subgrids(index: GridIndex, min_points: int = SUBGRID_MIN_POINTS) -> N
         return
     dev = index.X.device
     s = _lib.stream_handle()
-    v = index.view()
+    v = index.view(density=False)
     cap = n // (min_points + 1) + 1
     cells = torch.empty(cap, dtype=torch.int32, device=dev)
     cnt = torch.zeros(1, dtype=torch.int32, device=dev)
