@@ -42,6 +42,10 @@ enum { GHN_OK = 0, GHN_ERR_VALUE = 1, GHN_ERR_CUDA = 2, GHN_ERR_UNSUPPORTED = 3 
 const char *ghn_last_error(void);
 /* ABI version (major*100 + minor). */
 int32_t ghn_abi_version(void);
+/* Build flags: bit 0 = measurement knobs read from GHN_* environment
+ * variables (a -DGHN_TUNING_KNOBS build; the product build ignores the
+ * environment), bit 1 = per-site fallback counters (-DGHN_FB_REASONS). */
+int32_t ghn_build_flags(void);
 
 /* ------------------------------------------------------------------ fit
  * Replaces grid.build (grid.py:165-195) together with _hash_all

@@ -25,6 +25,7 @@ GHN_OK, GHN_ERR_VALUE, GHN_ERR_CUDA, GHN_ERR_UNSUPPORTED = 0, 1, 2, 3
 EXPORTS = (
     "ghn_last_error",
     "ghn_abi_version",
+    "ghn_build_flags",
     "ghn_fit_bounds",
     "ghn_fit_plan_init",
     "ghn_fit_build",
@@ -117,6 +118,7 @@ def lib():
     L = ctypes.CDLL(LIB_PATH)
     L.ghn_last_error.restype = ctypes.c_char_p
     L.ghn_abi_version.restype = _i32
+    L.ghn_build_flags.restype = _i32
     L.ghn_fit_bounds.argtypes = [_p, _i32, _i64, _i32, _p, _p, _p, _p, _p]
     L.ghn_fit_bounds.restype = _i32
     L.ghn_fit_plan_init.argtypes = [ctypes.POINTER(FitPlan), _i64, _i32, _i32, _p, _p, _i64]
@@ -179,3 +181,8 @@ def stream_handle(stream=None) -> int:
 
     s = stream if stream is not None else torch.cuda.current_stream()
     return int(s.cuda_stream)
+
+
+def tuning_build() -> bool:
+    """True when the library reads the GHN_* measurement knobs (tuning build)."""
+    return bool(lib().ghn_build_flags() & 1)

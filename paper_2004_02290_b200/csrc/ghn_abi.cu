@@ -52,6 +52,17 @@ int32_t cuda_status(cudaError_t e, const char *where) {
 
 extern "C" const char *ghn_last_error(void) { return ghn::g_last_error; }
 
-extern "C" int32_t ghn_abi_version(void) { return 100; }
+extern "C" int32_t ghn_abi_version(void) { return 200; }
+
+extern "C" int32_t ghn_build_flags(void) {
+    int32_t f = 0;
+#ifdef GHN_TUNING_KNOBS
+    f |= 1;
+#endif
+#ifdef GHN_FB_REASONS
+    f |= 2;
+#endif
+    return f;
+}
 
 extern "C" uint64_t ghn_launch_count(void) { return ghn::g_launches.load(); }

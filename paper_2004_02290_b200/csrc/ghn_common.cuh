@@ -196,6 +196,44 @@ __device__ __forceinline__ T warp_max(T v) {
 __device__ __forceinline__ double to_double(float x) { return (double)x; }
 __device__ __forceinline__ double to_double(double x) { return x; }
 
+// ---------------------------------------------------------------- TMA 1-D
+// Bulk global -> shared copies (cp.async.bulk, SASS UBLKCP) completing on a
+// CTA-local mbarrier: one thread arms the barrier with the byte count and
+// issues the copies; every thread waits on the phase.
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_parity(uint64_t *bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@!P1 bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+// bytes: multiple of 16; src / dst 16-byte aligned.
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+// Issue a copy of any 16-byte multiple in pieces of at most 32 KB.
+__device__ __forceinline__ void bulk_g2s_all(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+    for (uint32_t o = 0; o < bytes; o += 32768u) {
+        const uint32_t b = bytes - o < 32768u ? bytes - o : 32768u;
+        bulk_g2s((char *)dst + o, (const char *)src + o, b, bar);
+    }
+}
+
 // Order-preserving encoding of doubles into uint64 (for atomicMin).
 __device__ __forceinline__ unsigned long long dbl_order_key(double v) {
     unsigned long long b = (unsigned long long)__double_as_longlong(v);

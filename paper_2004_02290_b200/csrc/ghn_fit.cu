@@ -558,6 +558,366 @@ __global__ void __launch_bounds__(FIT_THREADS) fixup_records_kernel(
     }
 }
 
+// ------------------------------------------------------------------
+// Streaming fit (DENSE; the default when every key-range bucket fits a CTA).
+// Final buckets are runs of 2^shift consecutive cell keys (<= 32768 of
+// them, a few thousand points each).
+//   count  : points per final bucket (shared-memory histogram)   [read X]
+//   part1  : records (coords, label, index) by the bucket's top bits (<= 128
+//            level-1 buckets); each CTA counting-sorts an 8K-point chunk in
+//            shared memory and writes one contiguous run per level-1 bucket
+//                                                   [read X + labels, write records]
+//   part2  : the same over the level-1 output by the low 8 bits (a chunk
+//            spans <= 2 level-1 buckets, so <= 512 digits)  [read + write records]
+//   local  : one CTA per final bucket, entirely in shared memory: the
+//            bucket's records, cell histogram -> scan -> pt_off, slots
+//            grouped by cell, each cell's slots ordered by point index (the
+//            stable in-cell order of np.lexsort, grid.py:188-189), coalesced
+//            SoA coordinates / perm / labels            [read records, write outputs]
+// Every global write is a burst of consecutive records, so no HBM sector
+// is written partially (the scattered 16-byte writes of a one-level
+// partition into 8K buckets cost ~2x their bytes in read-modify-write).
+constexpr int SF_MAX_BUCKETS = 32768;
+constexpr int SF_L2_BITS = 8;
+constexpr int SF_MAX_L1 = SF_MAX_BUCKETS >> SF_L2_BITS;   // 128
+constexpr int SF_MAX_CELLS = 8192;       // cells per final bucket (shared histogram)
+constexpr int SF_COUNT_THREADS = 1024;
+constexpr int SF_PART_THREADS = 256;
+constexpr int SF_LOCAL_THREADS = 256;
+constexpr int SF_MAX_POINTS = 65535;     // per final bucket (16-bit record positions)
+
+template <typename T, int D>
+__device__ __forceinline__ uint32_t sf_key_d(const T (&x)[D > 0 ? D : 1], const DimParams &p) {
+    uint64_t key = 0;
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+        const int64_t c = cell_id(to_double(x[j]), p.w[j], p.inv[j], (p.pow2 >> j) & 1u);
+        key = key * (uint64_t)p.ext[j] + (uint64_t)(c - p.lo[j]);
+    }
+    return (uint32_t)key;
+}
+
+// Final-bucket histogram.  D > 0: compile-time dims, 4 points in flight per
+// thread; D == 0: point_key.
+template <typename T, int D>
+__global__ void __launch_bounds__(SF_COUNT_THREADS) sf_count_kernel(const T *__restrict__ X, int64_t n, DimParams p,
+                                                                   int shift, int nb, int32_t *__restrict__ bcount) {
+    extern __shared__ int sf_hist[];
+    for (int b = threadIdx.x; b < nb; b += blockDim.x) sf_hist[b] = 0;
+    __syncthreads();
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (D > 0) {
+        constexpr int DD = D > 0 ? D : 1;
+        constexpr int BU = 8;
+        for (; i + (BU - 1) * stride < n; i += BU * stride) {
+            T v[BU][DD];
+#pragma unroll
+            for (int u = 0; u < BU; ++u)
+#pragma unroll
+                for (int j = 0; j < DD; ++j) v[u][j] = __ldcs(X + (i + u * stride) * DD + j);
+#pragma unroll
+            for (int u = 0; u < BU; ++u) atomicAdd(&sf_hist[sf_key_d<T, DD>(v[u], p) >> shift], 1);
+        }
+    }
+    for (; i < n; i += stride) atomicAdd(&sf_hist[point_key<T, true>(X, i, p) >> shift], 1);
+    __syncthreads();
+    for (int b = threadIdx.x; b < nb; b += blockDim.x)
+        if (sf_hist[b]) atomicAdd(&bcount[b], sf_hist[b]);
+}
+
+template <int RWP>
+__device__ __forceinline__ void sf_load_record(const uint32_t *__restrict__ src, int64_t r, uint32_t (&w)[RWP]) {
+    const uint4 *q = reinterpret_cast<const uint4 *>(src + r * RWP);
+#pragma unroll
+    for (int t = 0; t < RWP / 4; ++t) {
+        const uint4 v = q[t];
+        w[4 * t] = v.x;
+        w[4 * t + 1] = v.y;
+        w[4 * t + 2] = v.z;
+        w[4 * t + 3] = v.w;
+    }
+}
+
+template <int RWP>
+__device__ __forceinline__ void sf_store_record(uint32_t *__restrict__ dst, int64_t r, const uint32_t (&w)[RWP]) {
+    uint4 *q = reinterpret_cast<uint4 *>(dst + r * RWP);
+#pragma unroll
+    for (int t = 0; t < RWP / 4; ++t) q[t] = make_uint4(w[4 * t], w[4 * t + 1], w[4 * t + 2], w[4 * t + 3]);
+}
+
+// Cell key of a record; the loop is unrolled to the most coordinates a
+// record of RWP words holds, so the record stays in registers.
+template <typename T, int RWP>
+__device__ __forceinline__ uint32_t sf_record_key(const uint32_t (&w)[RWP], const DimParams &p) {
+    constexpr int MAXD = (RWP - 2) * 4 / (int)sizeof(T);
+    uint64_t key = 0;
+#pragma unroll
+    for (int j = 0; j < MAXD; ++j) {
+        if (j < p.d) {
+            double x;
+            if (sizeof(T) == 4) x = (double)__uint_as_float(w[j]);
+            else x = __hiloint2double((int)w[2 * j + 1], (int)w[2 * j]);
+            const int64_t c = cell_id(x, p.w[j], p.inv[j], (p.pow2 >> j) & 1u);
+            key = key * (uint64_t)p.ext[j] + (uint64_t)(c - p.lo[j]);
+        }
+    }
+    return (uint32_t)key;
+}
+
+// Block-wide exclusive scan of a[0..len) in shared memory; returns the total.
+__device__ __forceinline__ int sf_block_scan(int *a, int len, int *warp_tot) {
+    const int per = (len + blockDim.x - 1) / blockDim.x;
+    const int b0 = threadIdx.x * per;
+    int sum = 0;
+    for (int t = 0; t < per; ++t)
+        if (b0 + t < len) sum += a[b0 + t];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int incl = warp_inclusive_scan(sum);
+    if (lane == 31) warp_tot[wid] = incl;
+    __syncthreads();
+    if (wid == 0) {
+        const int nw = (int)(blockDim.x >> 5);
+        const int v = lane < nw ? warp_tot[lane] : 0;
+        const int vi = warp_inclusive_scan(v);
+        if (lane < nw) warp_tot[lane] = vi - v;
+        if (lane == 31) warp_tot[32] = vi;
+    }
+    __syncthreads();
+    int run = incl - sum + warp_tot[wid];
+    for (int t = 0; t < per; ++t)
+        if (b0 + t < len) {
+            const int v = a[b0 + t];
+            a[b0 + t] = run;
+            run += v;
+        }
+    const int total = warp_tot[32];
+    __syncthreads();
+    return total;
+}
+
+// Level-2 chunks never straddle a level-1 bucket: chunk prefix per level-1
+// bucket (cpre[b1] = chunks before bucket b1), one warp.
+__global__ void sf_chunk_prefix_kernel(const int32_t *__restrict__ bbase, int nb, int nb1, int ch,
+                                       int32_t *__restrict__ cpre) {
+    int run = 0;
+    for (int b0 = 0; b0 < nb1; b0 += 32) {
+        const int b1 = b0 + (int)threadIdx.x;
+        int c = 0;
+        if (b1 < nb1) {
+            const int32_t st = bbase[b1 << SF_L2_BITS];
+            const int32_t en = bbase[min((b1 + 1) << SF_L2_BITS, nb)];
+            c = (en - st + ch - 1) / ch;
+        }
+        const int incl = warp_inclusive_scan(c);
+        if (b1 < nb1) cpre[b1] = run + incl - c;
+        run += __shfl_sync(GHN_FULL, incl, 31);
+    }
+    if (threadIdx.x == 0) cpre[nb1] = run;
+}
+
+// One level of the partition over a chunk of CH items, staged through shared
+// memory: the chunk's input arrives by 1-D TMA (cp.async.bulk) into the
+// staging area, each thread takes ITEMS items into registers with their
+// digit and rank (shared atomics), then the items are counting-sorted into
+// the staging area and every digit's run leaves in one burst of consecutive
+// 16-byte stores at [reserved base, ...).
+//   LEVEL 1: items = points of X (+ labels), digit = final bucket >> 8,
+//            chunk = blockIdx.x;
+//   LEVEL 2: items = level-1 records of one level-1 bucket b1 (chunks from
+//            cpre), digit = final bucket & 255.
+template <typename T, int RWP, int LEVEL, int ITEMS>
+__global__ void __launch_bounds__(SF_PART_THREADS) sf_part_kernel(const T *__restrict__ X, const int32_t *__restrict__ labels,
+                                                                 const uint32_t *__restrict__ in, int64_t n, DimParams p,
+                                                                 int shift, const int32_t *__restrict__ bbase,
+                                                                 const int32_t *__restrict__ cpre, int nb, int nb1,
+                                                                 int32_t *__restrict__ cursor,
+                                                                 uint32_t *__restrict__ out) {
+    constexpr int CH = ITEMS * SF_PART_THREADS;
+    constexpr int ND = LEVEL == 1 ? SF_MAX_L1 : (1 << SF_L2_BITS);
+    extern __shared__ uint4 sf_stage4[];
+    uint32_t *stage = reinterpret_cast<uint32_t *>(sf_stage4);       // CH records
+    uint16_t *sdig = reinterpret_cast<uint16_t *>(stage + CH * RWP);  // CH digits
+    __shared__ int cnt[ND], off[ND], gbase[ND];
+    __shared__ int warp_tot[33];
+    __shared__ int64_t s_i0, s_i1;
+    __shared__ int s_b1;
+    __shared__ alignas(8) uint64_t bar;
+    const int d = p.d;
+    if (threadIdx.x == 0) {
+        int64_t i0, i1;
+        int b1 = 0;
+        if (LEVEL == 1) {
+            i0 = (int64_t)blockIdx.x * CH;
+            i1 = i0 + CH < n ? i0 + CH : n;
+        } else {
+            // the level-1 bucket holding this chunk: last b1 with cpre[b1] <= blockIdx.x
+            int lo = 0, hi = nb1;
+            while (hi - lo > 1) {
+                const int mid = (lo + hi) >> 1;
+                if (cpre[mid] <= (int)blockIdx.x) lo = mid;
+                else hi = mid;
+            }
+            b1 = lo;
+            const int64_t st = bbase[b1 << SF_L2_BITS], en = bbase[min((b1 + 1) << SF_L2_BITS, nb)];
+            i0 = st + (int64_t)((int)blockIdx.x - cpre[b1]) * CH;
+            i1 = i0 + CH < en ? i0 + CH : en;
+            if ((int)blockIdx.x >= cpre[nb1]) i0 = i1 = 0;
+        }
+        s_i0 = i0;
+        s_i1 = i1;
+        s_b1 = b1;
+        mbar_init(&bar, 1);
+    }
+    for (int b = threadIdx.x; b < ND; b += blockDim.x) cnt[b] = 0;
+    __syncthreads();
+    const int64_t i0 = s_i0, i1 = s_i1;
+    const int m = (int)(i1 - i0);
+    if (m <= 0) return;
+    // ---- chunk input into the staging area (TMA when 16-byte sized)
+    const uint32_t xbytes = LEVEL == 1 ? (uint32_t)m * d * sizeof(T) : (uint32_t)m * RWP * 4;
+    const uint32_t lbytes = (LEVEL == 1 && labels) ? (uint32_t)m * 4 : 0u;
+    uint32_t *lab_s = stage + ((xbytes + 15) / 16) * 4;      // labels after the coordinates
+    const void *xsrc = LEVEL == 1 ? (const void *)(X + i0 * d) : (const void *)(in + i0 * RWP);
+    const bool bulk = xbytes % 16 == 0 && lbytes % 16 == 0;
+    if (bulk) {
+        if (threadIdx.x == 0) {
+            mbar_arrive_expect_tx(&bar, xbytes + lbytes);
+            bulk_g2s_all(stage, xsrc, xbytes, &bar);
+            if (lbytes) bulk_g2s_all(lab_s, labels + i0, lbytes, &bar);
+        }
+        mbar_wait_parity(&bar, 0);
+    } else {
+        for (uint32_t q = threadIdx.x; q < xbytes / 4; q += blockDim.x) stage[q] = ((const uint32_t *)xsrc)[q];
+        for (uint32_t q = threadIdx.x; q < lbytes / 4; q += blockDim.x) lab_s[q] = (uint32_t)labels[i0 + q];
+        __syncthreads();
+    }
+    const int cw = d * (int)(sizeof(T) / 4);
+    const int fb = LEVEL == 2 ? s_b1 << SF_L2_BITS : 0;
+    uint32_t w[ITEMS][RWP];
+    int dig[ITEMS], rank[ITEMS];
+#pragma unroll
+    for (int u = 0; u < ITEMS; ++u) {
+        const int t = threadIdx.x + u * SF_PART_THREADS;
+        dig[u] = -1;
+        if (t < m) {
+            if (LEVEL == 1) {
+#pragma unroll
+                for (int q = 0; q < RWP; ++q) w[u][q] = 0u;
+#pragma unroll
+                for (int q = 0; q < RWP - 2; ++q)
+                    if (q < cw) w[u][q] = stage[t * cw + q];
+                w[u][RWP - 2] = lbytes ? lab_s[t] : 0u;
+                w[u][RWP - 1] = (uint32_t)(i0 + t);
+                dig[u] = (int)((sf_record_key<T, RWP>(w[u], p) >> shift) >> SF_L2_BITS);
+            } else {
+#pragma unroll
+                for (int q = 0; q < RWP; ++q) w[u][q] = stage[t * RWP + q];
+                dig[u] = (int)(sf_record_key<T, RWP>(w[u], p) >> shift) - fb;
+            }
+            rank[u] = atomicAdd(&cnt[dig[u]], 1);
+        }
+    }
+    __syncthreads();   // the staging area's input is consumed
+    for (int b = threadIdx.x; b < ND; b += blockDim.x) off[b] = cnt[b];
+    __syncthreads();
+    sf_block_scan(off, ND, warp_tot);
+    for (int b = threadIdx.x; b < ND; b += blockDim.x) {
+        const int c = cnt[b];
+        gbase[b] = c ? atomicAdd(&cursor[fb + b], c) : 0;
+    }
+#pragma unroll
+    for (int u = 0; u < ITEMS; ++u)
+        if (dig[u] >= 0) {
+            const int sl = off[dig[u]] + rank[u];
+#pragma unroll
+            for (int q = 0; q < RWP; q += 4)
+                sf_stage4[(sl * RWP + q) / 4] = make_uint4(w[u][q], w[u][q + 1], w[u][q + 2], w[u][q + 3]);
+            sdig[sl] = (uint16_t)dig[u];
+        }
+    __syncthreads();
+    // RWP / 4 uint4 per record: consecutive threads store consecutive 16-byte words of a run
+    for (int q = threadIdx.x; q < m * (RWP / 4); q += blockDim.x) {
+        const int sl = q / (RWP / 4), part = q % (RWP / 4);
+        const int b = sdig[sl];
+        const int64_t g = (int64_t)gbase[b] + (sl - off[b]);
+        reinterpret_cast<uint4 *>(out + g * RWP)[part] = sf_stage4[q];
+    }
+}
+
+template <typename T, int RWP>
+__global__ void __launch_bounds__(SF_LOCAL_THREADS) sf_local_kernel(const uint32_t *__restrict__ part,
+                                                                   const int32_t *__restrict__ bbase, int shift,
+                                                                   int64_t E, int64_t n, DimParams p,
+                                                                   T *__restrict__ coords, int32_t *__restrict__ perm,
+                                                                   int32_t *__restrict__ labels_out,
+                                                                   int32_t *__restrict__ pt_off) {
+    extern __shared__ uint4 sf_lm4[];
+    __shared__ int warp_tot[33];
+    const int b = blockIdx.x;
+    const int32_t r0 = bbase[b], m = bbase[b + 1] - r0;
+    const int64_t c0 = (int64_t)b << shift;
+    const int ncell = (int)min((int64_t)1 << shift, E - c0);
+    uint32_t *rec = reinterpret_cast<uint32_t *>(sf_lm4);        // m records
+    int *hist = reinterpret_cast<int *>(rec + (size_t)m * RWP);     // ncell
+    uint16_t *spos = reinterpret_cast<uint16_t *>(hist + ncell);    // m record positions, grouped by cell
+    __shared__ alignas(8) uint64_t bar;
+    if (threadIdx.x == 0) {
+        mbar_init(&bar, 1);
+        if (m > 0) {   // the bucket's records by 1-D TMA
+            mbar_arrive_expect_tx(&bar, (uint32_t)m * RWP * 4);
+            bulk_g2s_all(rec, part + (int64_t)r0 * RWP, (uint32_t)m * RWP * 4, &bar);
+        }
+    }
+    for (int c = threadIdx.x; c < ncell; c += blockDim.x) hist[c] = 0;
+    __syncthreads();
+    if (m > 0) mbar_wait_parity(&bar, 0);
+    for (int t = threadIdx.x; t < m; t += blockDim.x) {
+        uint32_t w[RWP];
+#pragma unroll
+        for (int u = 0; u < RWP; ++u) w[u] = rec[t * RWP + u];
+        atomicAdd(&hist[sf_record_key<T, RWP>(w, p) - (uint32_t)c0], 1);
+    }
+    __syncthreads();
+    sf_block_scan(hist, ncell, warp_tot);
+    for (int c = threadIdx.x; c < ncell; c += blockDim.x) pt_off[c0 + c] = r0 + hist[c];
+    __syncthreads();
+    // positions grouped by cell (arbitrary order inside a cell); hist[c] ends as the end of cell c
+    for (int t = threadIdx.x; t < m; t += blockDim.x) {
+        uint32_t w[RWP];
+#pragma unroll
+        for (int u = 0; u < RWP; ++u) w[u] = rec[t * RWP + u];
+        spos[atomicAdd(&hist[sf_record_key<T, RWP>(w, p) - (uint32_t)c0], 1)] = (uint16_t)t;
+    }
+    __syncthreads();
+    // each cell's positions by point index (insertion sort; cells hold a few points)
+    for (int c = threadIdx.x; c < ncell; c += blockDim.x) {
+        const int s0 = c ? hist[c - 1] : 0, s1 = hist[c];
+        for (int s = s0 + 1; s < s1; ++s) {
+            const uint16_t kp = spos[s];
+            const uint32_t ki = rec[kp * RWP + RWP - 1];
+            int u = s - 1;
+            while (u >= s0 && rec[spos[u] * RWP + RWP - 1] > ki) {
+                spos[u + 1] = spos[u];
+                --u;
+            }
+            spos[u + 1] = kp;
+        }
+    }
+    __syncthreads();
+    const int d = p.d;
+    for (int s = threadIdx.x; s < m; s += blockDim.x) {
+        const uint32_t *w = rec + (size_t)spos[s] * RWP;
+        const T *xc = reinterpret_cast<const T *>(w);
+        const int64_t o = (int64_t)r0 + s;
+        for (int j = 0; j < d; ++j) __stcs(coords + (int64_t)j * n + o, xc[j]);
+        __stcs(perm + o, (int32_t)w[RWP - 1]);
+        if (labels_out) __stcs(labels_out + o, (int32_t)w[RWP - 2]);
+    }
+}
+
+__global__ void sf_tail_kernel(int32_t *pt_off, int64_t E, int64_t n) { pt_off[E] = (int32_t)n; }
+
 // Cell table from the offsets: non-empty flags -> (scan) -> cell_start / ids.
 __global__ void ne_flag_kernel(const int32_t *__restrict__ pt_off, int64_t E, int32_t *__restrict__ ne) {
     for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c <= E;
@@ -655,6 +1015,90 @@ int32_t bounds_launch(const T *X, int64_t n, int d, const DimParams &p, int64_t 
     return GHN_OK;
 }
 
+// Streaming fit host side (see sf_*): returns GHN_ERR_UNSUPPORTED without
+// touching the outputs when a final bucket spans too many cells or holds
+// more points than a CTA's shared memory takes.
+template <typename T, int RWP>
+int32_t fit_stream_rw(const ghn_fit_plan *plan, const T *X, const ghn_fit_out *out, char *ws, char *sws,
+                      const DimParams &p, cudaStream_t s) {
+    const int64_t n = plan->n, E = plan->E;
+    const int d = plan->d;
+    const int kb = plan->key_bits > 0 ? plan->key_bits : 1;
+    const int shift = kb > 15 ? kb - 15 : 0;
+    if (((int64_t)1 << shift) > SF_MAX_CELLS) return GHN_ERR_UNSUPPORTED;
+    const int nb = (int)(((E - 1) >> shift) + 1);
+    const int nb1 = ((nb - 1) >> SF_L2_BITS) + 1;
+    int32_t *bcount = (int32_t *)(ws + fast_bcur_off(plan));          // nb + 1: final bucket bases
+    int32_t *cur2 = bcount + align256((size_t)(nb + 1) * 4) / 4;      // nb: final bucket cursors
+    int32_t *cur1 = cur2 + align256((size_t)nb * 4) / 4;              // nb1: level-1 cursors
+    int32_t *dmax = cur1 + align256((size_t)SF_MAX_L1 * 4) / 4;
+    int32_t *cpre = dmax + 64;                                         // nb1 + 1
+    uint32_t *part1 = (uint32_t *)(ws + plan->fast_rec_off);
+    uint32_t *part2 = (uint32_t *)(ws + fast_part_off(plan));
+    GHN_CUDA_CHECK(cudaMemsetAsync(bcount, 0, (size_t)(nb + 1) * 4, s));
+    GHN_CUDA_CHECK(cudaMemsetAsync(dmax, 0, 4, s));
+    const size_t csmem = (size_t)nb * 4;
+    const void *cfn = d == 2 ? (const void *)sf_count_kernel<T, 2> : (const void *)sf_count_kernel<T, 0>;
+    GHN_CUDA_CHECK(cudaFuncSetAttribute(cfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csmem));
+    const unsigned cg = (unsigned)sm_count() * (csmem > 64 * 1024 ? 1 : 2);
+    if (d == 2)
+        sf_count_kernel<T, 2><<<cg, SF_COUNT_THREADS, csmem, s>>>(X, n, p, shift, nb, bcount);
+    else
+        sf_count_kernel<T, 0><<<cg, SF_COUNT_THREADS, csmem, s>>>(X, n, p, shift, nb, bcount);
+    GHN_LAUNCH_CHECK("sf_count_kernel");
+    int32_t rc = exclusive_scan_i32(bcount, bcount, nb + 1, sws, s);
+    if (rc) return rc;
+    max_count_kernel<<<grid_for(nb), FIT_THREADS, 0, s>>>(bcount, nb, dmax);
+    GHN_LAUNCH_CHECK("max_count_kernel");
+    int32_t hmax = 0;
+    GHN_CUDA_CHECK(cudaMemcpyAsync(&hmax, dmax, 4, cudaMemcpyDeviceToHost, s));
+    GHN_CUDA_CHECK(cudaStreamSynchronize(s));
+    const int ncell = (int)((int64_t)1 << shift);
+    const size_t lsmem = (size_t)hmax * (RWP * 4 + 2) + (size_t)ncell * 4 + 64;
+    if (hmax > SF_MAX_POINTS || lsmem > 200 * 1024) return GHN_ERR_UNSUPPORTED;
+    // cursors: final buckets from their bases, level-1 buckets from their first final bucket's base
+    GHN_CUDA_CHECK(cudaMemcpyAsync(cur2, bcount, (size_t)nb * 4, cudaMemcpyDeviceToDevice, s));
+    GHN_CUDA_CHECK(cudaMemcpy2DAsync(cur1, 4, bcount, (size_t)4 << SF_L2_BITS, 4, nb1, cudaMemcpyDeviceToDevice, s));
+    constexpr int IT = RWP == 4 ? 8 : 4;
+    constexpr int CH = IT * SF_PART_THREADS;
+    sf_chunk_prefix_kernel<<<1, 32, 0, s>>>(bcount, nb, nb1, CH, cpre);
+    GHN_LAUNCH_CHECK("sf_chunk_prefix_kernel");
+    const size_t psmem = (size_t)CH * (RWP * 4 + 2);
+    const unsigned gp = (unsigned)((n + CH - 1) / CH);
+    const void *p1 = (const void *)sf_part_kernel<T, RWP, 1, IT>;
+    const void *p2 = (const void *)sf_part_kernel<T, RWP, 2, IT>;
+    const void *lf = (const void *)sf_local_kernel<T, RWP>;
+    GHN_CUDA_CHECK(cudaFuncSetAttribute(p1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem));
+    GHN_CUDA_CHECK(cudaFuncSetAttribute(p2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem));
+    GHN_CUDA_CHECK(cudaFuncSetAttribute(lf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lsmem));
+    sf_part_kernel<T, RWP, 1, IT><<<gp, SF_PART_THREADS, psmem, s>>>(X, out->labels_in, nullptr, n, p, shift, bcount,
+                                                                     cpre, nb, nb1, cur1, part1);
+    GHN_LAUNCH_CHECK("sf_part_kernel<1>");
+    sf_part_kernel<T, RWP, 2, IT><<<gp + nb1, SF_PART_THREADS, psmem, s>>>(X, nullptr, part1, n, p, shift, bcount,
+                                                                           cpre, nb, nb1, cur2, part2);
+    GHN_LAUNCH_CHECK("sf_part_kernel<2>");
+    sf_local_kernel<T, RWP><<<nb, SF_LOCAL_THREADS, lsmem, s>>>(part2, bcount, shift, E, n, p, (T *)out->coords,
+                                                                out->perm, out->labels_perm, out->pt_off);
+    GHN_LAUNCH_CHECK("sf_local_kernel");
+    sf_tail_kernel<<<1, 1, 0, s>>>(out->pt_off, E, n);
+    GHN_LAUNCH_CHECK("sf_tail_kernel");
+    ne_flag_kernel<<<grid_for(E + 1), FIT_THREADS, 0, s>>>(out->pt_off, E, out->ne_off);
+    GHN_LAUNCH_CHECK("ne_flag_kernel");
+    rc = exclusive_scan_i32(out->ne_off, out->ne_off, E + 1, sws, s);
+    if (rc) return rc;
+    cells_from_offsets_kernel<<<grid_for(E), FIT_THREADS, 0, s>>>(out->pt_off, out->ne_off, E, n, p, out->cell_start,
+                                                                  out->cell_ids, out->n_cells);
+    GHN_LAUNCH_CHECK("cells_from_offsets_kernel");
+    return GHN_OK;
+}
+
+template <typename T>
+int32_t fit_stream(const ghn_fit_plan *plan, const T *X, const ghn_fit_out *out, char *ws, char *sws,
+                   const DimParams &p, cudaStream_t s) {
+    if (part_words(plan->d, plan->dtype) == 4) return fit_stream_rw<T, 4>(plan, X, out, ws, sws, p, s);
+    return fit_stream_rw<T, 8>(plan, X, out, ws, sws, p, s);
+}
+
 template <typename T>
 int32_t fit_build_impl(const ghn_fit_plan *plan, const T *X, const ghn_fit_out *out, char *ws,
                        size_t ws_bytes, cudaStream_t s) {
@@ -674,6 +1118,10 @@ int32_t fit_build_impl(const ghn_fit_plan *plan, const T *X, const ghn_fit_out *
     int32_t rc;
 
     const int RW = record_words(d, plan->dtype);
+    if (plan->layout == GHN_LAYOUT_DENSE && RW > 0 && knob("GHN_FIT_STREAM", 1) != 0) {
+        rc = fit_stream(plan, X, out, ws, sws, p, s);
+        if (rc != GHN_ERR_UNSUPPORTED) return rc;   // unsupported: a bucket too large, use the chain below
+    }
     if (plan->layout == GHN_LAYOUT_DENSE && RW > 0) {
         // counting scatter: histogram into pt_off[0..E), scan in place (E+1)
         const int64_t E = plan->E;
@@ -896,7 +1344,8 @@ extern "C" int32_t ghn_fit_plan_init(ghn_fit_plan *plan, int64_t n, int32_t d, i
         const size_t base = 5 * n4 + align256(radix_workspace_bytes(n)) + align256(scan_workspace_bytes(scan_len));
         plan->fast_cursor_off = base;
         plan->fast_rec_off = base + align256((size_t)(plan->E + 1) * 4);
-        const size_t need = fast_bcur_off(plan) + align256((size_t)PART_BUCKETS * 4);
+        // bucket cursors (chain) / streaming-fit bucket counts, cursors, max
+        const size_t need = fast_bcur_off(plan) + 4 * align256((size_t)(SF_MAX_BUCKETS + 1) * 4);
         if (need > plan->workspace_bytes) plan->workspace_bytes = need;
     }
     return GHN_OK;

@@ -124,7 +124,7 @@ def _run(index: GridIndex, Qt, k, mode, task, want_neighbors, want_stats, want_t
             raise ValueError("labels are not numeric targets")
         res["value"] = torch.empty(nq, dtype=torch.float64, device=dev)
         out.value = _lib.ptr(res["value"])
-    view = index.view()
+    view = index.view(targets=task in (_lib.GHN_TASK_REGRESS_MEAN, _lib.GHN_TASK_REGRESS_MEDIAN))
     if qorder is not None:
         wsz, ws = 0, None
     else:
@@ -175,7 +175,7 @@ def query_order(index: GridIndex, Q, stream=None):
         Qd = Qd.to(torch.float64)
     nq = int(Qd.shape[0])
     qdt = _lib.GHN_F32 if Qd.dtype == torch.float32 else _lib.GHN_F64
-    view = index.view()
+    view = index.view(targets=False)
     wsz = int(L.ghn_query_workspace_size(ctypes.byref(view), nq, 1))
     ws = torch.empty(wsz, dtype=torch.uint8, device=Qd.device)
     order = torch.empty(nq, dtype=torch.int32, device=Qd.device)

@@ -231,9 +231,10 @@ class GridIndex:
         return self._cache["table"]
 
     # -- device view ----------------------------------------------------------
-    def view(self, density: bool = True) -> _lib.IndexView:
+    def view(self, density: bool = True, targets: bool = True) -> _lib.IndexView:
         """ctypes ghn_index_view of the device tables (density=False skips
-        the tiled predict's density hint, which costs a kernel + sync once)."""
+        the tiled predict's density hint, which costs a kernel + sync once;
+        targets=False leaves the fp64 regression targets unmaterialised)."""
         v = _lib.IndexView()
         p = self.plan
         v.n, v.d, v.dtype, v.layout, v.n_cells, v.E = p.n, p.d, p.dtype, p.layout, self.n_cells, p.E
@@ -249,7 +250,7 @@ class GridIndex:
         v.pt_off = _lib.ptr(self.pt_off)
         v.ne_off = _lib.ptr(self.ne_off)
         v.labels = _lib.ptr(self._labels.codes)
-        v.targets = _lib.ptr(self._labels.targets)
+        v.targets = _lib.ptr(self._labels.targets) if targets else 0
         v.labels_perm = _lib.ptr(self.labels_perm)
         v.n_labels = self._labels.n_codes
         v.metric = _lib.GHN_METRIC[self.metric]
@@ -454,7 +455,7 @@ def _build_subgrids(index: GridIndex, min_points: int = SUBGRID_MIN_POINTS) -> N
         return
     dev = index.X.device
     s = _lib.stream_handle()
-    v = index.view(density=False)
+    v = index.view(density=False, targets=False)
     cap = n // (min_points + 1) + 1
     cells = torch.empty(cap, dtype=torch.int32, device=dev)
     cnt = torch.zeros(1, dtype=torch.int32, device=dev)

@@ -128,18 +128,20 @@ def test_cfg1_cfg2_generic_kernel(ghn, cfg, nq):
     _check_knn(ghn, index, ref, w.Q[:200], w.k, "heuristic")
 
 
-@pytest.mark.parametrize("G", ["8", "16", "32"])
+@pytest.mark.parametrize("n_labels", [4, 20])
 @pytest.mark.parametrize("k", [1, 5, 16])
-def test_tiled_group_sizes_exact(ghn, G, k, monkeypatch):
-    """Every lanes-per-query variant of the tiled kernel (GHN_TILE_G) is exact."""
+def test_tiled_kernel_variants_exact(ghn, n_labels, k):
+    """The tiled kernel variants the plan picks (tile2d_plan): thread per
+    query for <= 8 label codes, 8-lane groups for k = 1 with <= 32 codes,
+    the warp kernel otherwise -- all exact, both stop modes."""
     from paper_2004_02290_b200 import datagen
 
-    monkeypatch.setenv("GHN_TILE_G", G)
     w = datagen.cfg4(n=1_000_000, nq=60_000, seed=45)
-    index = ghn.build_arrays(w.X, w.y, cells_per_axis=512)
+    y = (w.y if n_labels == 4 else np.random.default_rng(46).integers(0, n_labels, w.X.shape[0])).astype(np.int32)
+    index = ghn.build_arrays(w.X, y, cells_per_axis=512)
     ref = oracle.COracle(w.X, np.full(2, 1.0 / 512))
-    _check_predict(ghn, index, ref, w.X, w.y, w.Q, k, "heuristic")
-    _check_predict(ghn, index, ref, w.X, w.y, w.Q[:20000], k, "guaranteed")
+    _check_predict(ghn, index, ref, w.X, y, w.Q, k, "heuristic")
+    _check_predict(ghn, index, ref, w.X, y, w.Q[:20000], k, "guaranteed")
 
 
 @pytest.mark.parametrize("n_labels", [2, 40, 200, 300])

@@ -63,6 +63,8 @@ def test_fp64_queries(ghn, case, k):
 
 
 @pytest.mark.parametrize("k", [1, 4, 9, 16, 32])
+@pytest.mark.skipif("not __import__('paper_2004_02290_b200._lib', fromlist=['x']).tuning_build()",
+                    reason="GHN_TT_LISTMAX is a knob of the -DGHN_TUNING_KNOBS build only")
 def test_bucket_select_for_small_k(ghn, case, k, monkeypatch):
     """The bucket select is exact for every k, not only the k > 32 it serves."""
     monkeypatch.setenv("GHN_TT_LISTMAX", "0")
@@ -72,6 +74,8 @@ def test_bucket_select_for_small_k(ghn, case, k, monkeypatch):
 
 @pytest.mark.parametrize("k", [40, 64, 100])
 @pytest.mark.parametrize("mode", ["heuristic", "guaranteed"])
+@pytest.mark.skipif("not __import__('paper_2004_02290_b200._lib', fromlist=['x']).tuning_build()",
+                    reason="GHN_SB_RECAP is a knob of the -DGHN_TUNING_KNOBS build only")
 def test_reselect_over_255_candidates(ghn, case, k, mode, monkeypatch):
     """Re-selects over more than 255 candidates (GHN_SB_RECAP raised): the
     byte histogram may carry between buckets; the decoded-total check must
