@@ -29,6 +29,11 @@ struct DimParams {
     int64_t ext[GHN_MAX_DIM];
     uint32_t pow2;   // bit j: widths[j] is a power of two
     int32_t d;
+    // bit j: fp32 coordinates get their id as floor(x * inv) in fp32 --
+    // identical to the fp64 division: 1/w is a power of two >= 1, so the
+    // product is exact in fp32 (no rounding, no underflow) and |id| < 2^30
+    uint32_t fast32;
+    float inv32[GHN_MAX_DIM];
 };
 
 static DimParams make_dims(int d, const double *widths, const int64_t *lo, const int64_t *ext) {
@@ -44,6 +49,11 @@ static DimParams make_dims(int d, const double *widths, const int64_t *lo, const
         }
         if (lo) p.lo[j] = lo[j];
         if (ext) p.ext[j] = ext[j];
+        if (lo && ext && ((p.pow2 >> j) & 1u) && inv >= 1.0 && inv <= 0x1p100 && lo[j] > -(1LL << 30) &&
+            lo[j] + ext[j] < (1LL << 30)) {
+            p.fast32 |= 1u << j;
+            p.inv32[j] = (float)inv;
+        }
     }
     return p;
 }
@@ -586,12 +596,19 @@ constexpr int SF_PART_THREADS = 256;
 constexpr int SF_LOCAL_THREADS = 256;
 constexpr int SF_MAX_POINTS = 65535;     // per final bucket (16-bit record positions)
 
+// Cell id of a coordinate of the training set (inside [lo, hi] by construction).
+template <typename T>
+__device__ __forceinline__ int64_t fit_cell_id(T x, const DimParams &p, int j) {
+    if (sizeof(T) == 4 && ((p.fast32 >> j) & 1u)) return (int64_t)__float2int_rd((float)x * p.inv32[j]);
+    return cell_id(to_double(x), p.w[j], p.inv[j], (p.pow2 >> j) & 1u);
+}
+
 template <typename T, int D>
 __device__ __forceinline__ uint32_t sf_key_d(const T (&x)[D > 0 ? D : 1], const DimParams &p) {
     uint64_t key = 0;
 #pragma unroll
     for (int j = 0; j < D; ++j) {
-        const int64_t c = cell_id(to_double(x[j]), p.w[j], p.inv[j], (p.pow2 >> j) & 1u);
+        const int64_t c = fit_cell_id<T>(x[j], p, j);
         key = key * (uint64_t)p.ext[j] + (uint64_t)(c - p.lo[j]);
     }
     return (uint32_t)key;
@@ -655,10 +672,9 @@ __device__ __forceinline__ uint32_t sf_record_key(const uint32_t (&w)[RWP], cons
 #pragma unroll
     for (int j = 0; j < MAXD; ++j) {
         if (j < p.d) {
-            double x;
-            if (sizeof(T) == 4) x = (double)__uint_as_float(w[j]);
-            else x = __hiloint2double((int)w[2 * j + 1], (int)w[2 * j]);
-            const int64_t c = cell_id(x, p.w[j], p.inv[j], (p.pow2 >> j) & 1u);
+            int64_t c;
+            if (sizeof(T) == 4) c = fit_cell_id<float>(__uint_as_float(w[j]), p, j);
+            else c = fit_cell_id<double>(__hiloint2double((int)w[2 * j + 1], (int)w[2 * j]), p, j);
             key = key * (uint64_t)p.ext[j] + (uint64_t)(c - p.lo[j]);
         }
     }
@@ -727,7 +743,7 @@ __global__ void sf_chunk_prefix_kernel(const int32_t *__restrict__ bbase, int nb
 //   LEVEL 2: items = level-1 records of one level-1 bucket b1 (chunks from
 //            cpre), digit = final bucket & 255.
 template <typename T, int RWP, int LEVEL, int ITEMS>
-__global__ void __launch_bounds__(SF_PART_THREADS) sf_part_kernel(const T *__restrict__ X, const int32_t *__restrict__ labels,
+__global__ void __launch_bounds__(SF_PART_THREADS, 4) sf_part_kernel(const T *__restrict__ X, const int32_t *__restrict__ labels,
                                                                  const uint32_t *__restrict__ in, int64_t n, DimParams p,
                                                                  int shift, const int32_t *__restrict__ bbase,
                                                                  const int32_t *__restrict__ cpre, int nb, int nb1,
@@ -804,15 +820,27 @@ __global__ void __launch_bounds__(SF_PART_THREADS) sf_part_kernel(const T *__res
             if (LEVEL == 1) {
 #pragma unroll
                 for (int q = 0; q < RWP; ++q) w[u][q] = 0u;
+                if (cw == 2) {
+                    const uint2 v = reinterpret_cast<const uint2 *>(stage)[t];
+                    w[u][0] = v.x;
+                    w[u][1] = v.y;
+                } else {
 #pragma unroll
-                for (int q = 0; q < RWP - 2; ++q)
-                    if (q < cw) w[u][q] = stage[t * cw + q];
+                    for (int q = 0; q < RWP - 2; ++q)
+                        if (q < cw) w[u][q] = stage[t * cw + q];
+                }
                 w[u][RWP - 2] = lbytes ? lab_s[t] : 0u;
                 w[u][RWP - 1] = (uint32_t)(i0 + t);
                 dig[u] = (int)((sf_record_key<T, RWP>(w[u], p) >> shift) >> SF_L2_BITS);
             } else {
 #pragma unroll
-                for (int q = 0; q < RWP; ++q) w[u][q] = stage[t * RWP + q];
+                for (int q = 0; q < RWP; q += 4) {
+                    const uint4 v = sf_stage4[(t * RWP + q) / 4];
+                    w[u][q] = v.x;
+                    w[u][q + 1] = v.y;
+                    w[u][q + 2] = v.z;
+                    w[u][q + 3] = v.w;
+                }
                 dig[u] = (int)(sf_record_key<T, RWP>(w[u], p) >> shift) - fb;
             }
             rank[u] = atomicAdd(&cnt[dig[u]], 1);
@@ -875,7 +903,10 @@ __global__ void __launch_bounds__(SF_LOCAL_THREADS) sf_local_kernel(const uint32
     for (int t = threadIdx.x; t < m; t += blockDim.x) {
         uint32_t w[RWP];
 #pragma unroll
-        for (int u = 0; u < RWP; ++u) w[u] = rec[t * RWP + u];
+        for (int u = 0; u < RWP; u += 4) {
+            const uint4 v = sf_lm4[(t * RWP + u) / 4];
+            w[u] = v.x, w[u + 1] = v.y, w[u + 2] = v.z, w[u + 3] = v.w;
+        }
         atomicAdd(&hist[sf_record_key<T, RWP>(w, p) - (uint32_t)c0], 1);
     }
     __syncthreads();
@@ -886,7 +917,10 @@ __global__ void __launch_bounds__(SF_LOCAL_THREADS) sf_local_kernel(const uint32
     for (int t = threadIdx.x; t < m; t += blockDim.x) {
         uint32_t w[RWP];
 #pragma unroll
-        for (int u = 0; u < RWP; ++u) w[u] = rec[t * RWP + u];
+        for (int u = 0; u < RWP; u += 4) {
+            const uint4 v = sf_lm4[(t * RWP + u) / 4];
+            w[u] = v.x, w[u + 1] = v.y, w[u + 2] = v.z, w[u + 3] = v.w;
+        }
         spos[atomicAdd(&hist[sf_record_key<T, RWP>(w, p) - (uint32_t)c0], 1)] = (uint16_t)t;
     }
     __syncthreads();
