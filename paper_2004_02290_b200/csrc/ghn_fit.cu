@@ -593,7 +593,10 @@ constexpr int SF_MAX_L1 = SF_MAX_BUCKETS >> SF_L2_BITS;   // 128
 constexpr int SF_MAX_CELLS = 8192;       // cells per final bucket (shared histogram)
 constexpr int SF_COUNT_THREADS = 1024;
 constexpr int SF_PART_THREADS = 256;
-constexpr int SF_LOCAL_THREADS = 256;
+#ifndef SF_LOCAL_THR
+#define SF_LOCAL_THR 512
+#endif
+constexpr int SF_LOCAL_THREADS = SF_LOCAL_THR;
 constexpr int SF_MAX_POINTS = 65535;     // per final bucket (16-bit record positions)
 
 // Cell id of a coordinate of the training set (inside [lo, hi] by construction).
@@ -888,7 +891,8 @@ __global__ void __launch_bounds__(SF_LOCAL_THREADS) sf_local_kernel(const uint32
     const int ncell = (int)min((int64_t)1 << shift, E - c0);
     uint32_t *rec = reinterpret_cast<uint32_t *>(sf_lm4);        // m records
     int *hist = reinterpret_cast<int *>(rec + (size_t)m * RWP);     // ncell
-    uint16_t *spos = reinterpret_cast<uint16_t *>(hist + ncell);    // m record positions, grouped by cell
+    int32_t *sidx = hist + ncell;                                   // m point indices, grouped by cell
+    uint16_t *spos = reinterpret_cast<uint16_t *>(sidx + m);        // m record positions, grouped by cell
     __shared__ alignas(8) uint64_t bar;
     if (threadIdx.x == 0) {
         mbar_init(&bar, 1);
@@ -900,41 +904,48 @@ __global__ void __launch_bounds__(SF_LOCAL_THREADS) sf_local_kernel(const uint32
     for (int c = threadIdx.x; c < ncell; c += blockDim.x) hist[c] = 0;
     __syncthreads();
     if (m > 0) mbar_wait_parity(&bar, 0);
-    for (int t = threadIdx.x; t < m; t += blockDim.x) {
-        uint32_t w[RWP];
+    auto load = [&](int t, uint32_t (&w)[RWP]) {
 #pragma unroll
         for (int u = 0; u < RWP; u += 4) {
             const uint4 v = sf_lm4[(t * RWP + u) / 4];
             w[u] = v.x, w[u + 1] = v.y, w[u + 2] = v.z, w[u + 3] = v.w;
         }
+    };
+    for (int t = threadIdx.x; t < m; t += blockDim.x) {
+        uint32_t w[RWP];
+        load(t, w);
         atomicAdd(&hist[sf_record_key<T, RWP>(w, p) - (uint32_t)c0], 1);
     }
     __syncthreads();
     sf_block_scan(hist, ncell, warp_tot);
     for (int c = threadIdx.x; c < ncell; c += blockDim.x) pt_off[c0 + c] = r0 + hist[c];
     __syncthreads();
-    // positions grouped by cell (arbitrary order inside a cell); hist[c] ends as the end of cell c
+    // records grouped by cell (arbitrary order inside a cell); hist[c] ends as the end of cell c
     for (int t = threadIdx.x; t < m; t += blockDim.x) {
         uint32_t w[RWP];
-#pragma unroll
-        for (int u = 0; u < RWP; u += 4) {
-            const uint4 v = sf_lm4[(t * RWP + u) / 4];
-            w[u] = v.x, w[u + 1] = v.y, w[u + 2] = v.z, w[u + 3] = v.w;
-        }
-        spos[atomicAdd(&hist[sf_record_key<T, RWP>(w, p) - (uint32_t)c0], 1)] = (uint16_t)t;
+        load(t, w);
+        const int slot = atomicAdd(&hist[sf_record_key<T, RWP>(w, p) - (uint32_t)c0], 1);
+        sidx[slot] = (int32_t)w[RWP - 1];
+        spos[slot] = (uint16_t)t;
     }
     __syncthreads();
-    // each cell's positions by point index (insertion sort; cells hold a few points)
+#ifndef SF_SORT
+#define SF_SORT 1
+#endif
+#if SF_SORT
+    // each cell's slots by point index (insertion sort; cells hold a few points)
     for (int c = threadIdx.x; c < ncell; c += blockDim.x) {
         const int s0 = c ? hist[c - 1] : 0, s1 = hist[c];
         for (int s = s0 + 1; s < s1; ++s) {
+            const int32_t ki = sidx[s];
             const uint16_t kp = spos[s];
-            const uint32_t ki = rec[kp * RWP + RWP - 1];
             int u = s - 1;
-            while (u >= s0 && rec[spos[u] * RWP + RWP - 1] > ki) {
+            while (u >= s0 && sidx[u] > ki) {
+                sidx[u + 1] = sidx[u];
                 spos[u + 1] = spos[u];
                 --u;
             }
+            sidx[u + 1] = ki;
             spos[u + 1] = kp;
         }
     }
@@ -945,9 +956,28 @@ __global__ void __launch_bounds__(SF_LOCAL_THREADS) sf_local_kernel(const uint32
         const T *xc = reinterpret_cast<const T *>(w);
         const int64_t o = (int64_t)r0 + s;
         for (int j = 0; j < d; ++j) __stcs(coords + (int64_t)j * n + o, xc[j]);
-        __stcs(perm + o, (int32_t)w[RWP - 1]);
+        __stcs(perm + o, sidx[s]);
         if (labels_out) __stcs(labels_out + o, (int32_t)w[RWP - 2]);
     }
+#else
+    // slot s goes to its cell's start + its rank by point index inside the
+    // cell (the stable in-cell order of np.lexsort, grid.py:188-189)
+    const int d = p.d;
+    for (int s = threadIdx.x; s < m; s += blockDim.x) {
+        uint32_t w[RWP];
+        load(spos[s], w);
+        const int c = (int)(sf_record_key<T, RWP>(w, p) - (uint32_t)c0);
+        const int s0 = c ? hist[c - 1] : 0, s1 = hist[c];
+        const int32_t me = sidx[s];
+        int rank = 0;
+        for (int u = s0; u < s1; ++u) rank += sidx[u] < me;
+        const T *xc = reinterpret_cast<const T *>(w);
+        const int64_t o = (int64_t)r0 + s0 + rank;
+        for (int j = 0; j < d; ++j) __stcs(coords + (int64_t)j * n + o, xc[j]);
+        __stcs(perm + o, me);
+        if (labels_out) __stcs(labels_out + o, (int32_t)w[RWP - 2]);
+    }
+#endif
 }
 
 __global__ void sf_tail_kernel(int32_t *pt_off, int64_t E, int64_t n) { pt_off[E] = (int32_t)n; }
@@ -1088,7 +1118,7 @@ int32_t fit_stream_rw(const ghn_fit_plan *plan, const T *X, const ghn_fit_out *o
     GHN_CUDA_CHECK(cudaMemcpyAsync(&hmax, dmax, 4, cudaMemcpyDeviceToHost, s));
     GHN_CUDA_CHECK(cudaStreamSynchronize(s));
     const int ncell = (int)((int64_t)1 << shift);
-    const size_t lsmem = (size_t)hmax * (RWP * 4 + 2) + (size_t)ncell * 4 + 64;
+    const size_t lsmem = (size_t)hmax * (RWP * 4 + 6) + (size_t)ncell * 4 + 64;
     if (hmax > SF_MAX_POINTS || lsmem > 200 * 1024) return GHN_ERR_UNSUPPORTED;
     // cursors: final buckets from their bases, level-1 buckets from their first final bucket's base
     GHN_CUDA_CHECK(cudaMemcpyAsync(cur2, bcount, (size_t)nb * 4, cudaMemcpyDeviceToDevice, s));
