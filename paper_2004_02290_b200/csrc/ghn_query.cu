@@ -75,6 +75,10 @@ static size_t order_workspace_bytes(int64_t nq) {
 
 extern "C" size_t ghn_query_workspace_size(const ghn_index_view *ix, int64_t nq, int32_t k) {
     size_t b = order_workspace_bytes(nq);
+    if (k > 256) {
+        const size_t lk = largek_workspace_bytes(ix, k);
+        return lk > b ? lk : b;
+    }
     Tile2dPlan tp;
     if (tile2d_plan(ix, nq, k, GHN_TASK_CLASSIFY, false, &tp)) {
         size_t t = tile2d_workspace_bytes(&tp, nq);
@@ -91,10 +95,6 @@ static int32_t validate_query(const ghn_index_view *ix, int32_t k, int32_t mode)
     if (k < 1 || k > ix->n) {
         set_error("k=%d out of range [1, %lld]", k, (long long)ix->n);
         return GHN_ERR_VALUE;
-    }
-    if (k > 256) {
-        set_error("k=%d > 256 is not supported by the device top-k", k);
-        return GHN_ERR_UNSUPPORTED;
     }
     if (ix->d < 1 || ix->d > GHN_MAX_DIM) {
         set_error("d=%d unsupported", ix->d);
@@ -179,6 +179,7 @@ extern "C" int32_t ghn_query(const ghn_index_view *ix, const void *Q, int32_t q_
     a.out = *out;
     a.qorder = qorder;
     a.nq_dev = nullptr;
+    if (k > 256) return largek_query(ix, Q, q_dtype, nq, k, mode, task, out, workspace, workspace_bytes, s);
     const int ks = k <= 32 ? 1 : (k <= 64 ? 2 : (k <= 128 ? 4 : 8));
     Tile2dPlan tp;
     const bool want_nb = out->dist != nullptr || out->idx != nullptr;

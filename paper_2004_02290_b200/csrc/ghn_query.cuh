@@ -31,4 +31,10 @@ struct QArgs {
 int32_t launch_query_f32(const QArgs &a, int ks, cudaStream_t s);
 int32_t launch_query_f64(const QArgs &a, int ks, cudaStream_t s);
 
+// k > 256 (ghn_largek.cu): exact, one query and one layer at a time.
+size_t largek_workspace_bytes(const ghn_index_view *ix, int32_t k);
+int32_t largek_query(const ghn_index_view *ix, const void *Q, int32_t q_dtype, int64_t nq, int32_t k, int32_t mode,
+                     int32_t task, const ghn_query_out *out, void *workspace, size_t workspace_bytes,
+                     cudaStream_t s);
+
 }  // namespace ghn

@@ -20,6 +20,8 @@ from .core import Neighbor
 from .grid import CellId, GridIndex
 
 STOP_MODES = ("heuristic", "guaranteed")
+# Largest k the batched warp-resident top-k serves; larger k (any k <= n, as
+# explore.py:86-88 allows) run the exact per-query path (csrc/ghn_largek.cu).
 MAX_K = 256
 
 
@@ -78,8 +80,6 @@ def _validate_queries(index: GridIndex, Q, k: int):
     n = index.size
     if not 1 <= k <= n:
         raise ValueError(f"k={k} out of range [1, {n}]")
-    if k > MAX_K:
-        raise NotImplementedError(f"k={k} > {MAX_K} is not supported by the device top-k")
     return Qt
 
 

@@ -505,6 +505,16 @@ def _build_subgrids(index: GridIndex, min_points: int = SUBGRID_MIN_POINTS) -> N
                        "records": recs}
 
 
+def _max_splits_1d(values, cap):
+    """(splits, width) of one dimension (grid.py:52-82), on the device: the
+    max-splits width fit of the column as an (n, 1) matrix."""
+    from .fitwidths import fit_cell_measurements_arrays
+
+    v = np.asarray(values, dtype=np.float64).reshape(-1, 1)
+    params = fit_cell_measurements_arrays(v, cap)
+    return int(params.splits[0]), float(params.widths[0])
+
+
 def cell_points(index: GridIndex, cell) -> list[int]:
     """Point indices of one cell, empty for absent cells (grid.py:198-201)."""
     bucket = index.table.get(tuple(int(v) for v in cell))
