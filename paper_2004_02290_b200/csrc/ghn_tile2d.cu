@@ -1175,16 +1175,41 @@ bool tile2d_plan(const ghn_index_view *ix, int64_t nq, int32_t k, int32_t task, 
     }
     // staged-point capacity: the expected window plus margin (an overflowing
     // tile sends its queries to the generic kernel)
-    const double expect = (double)plan->win * plan->win * rho;
-    int cap = (int)(1.1 * expect + 64.0);   // Poisson window count: +10 % is > 5 sigma at cfg4
-    cap = (cap + 127) & ~127;
-    if (cap > 8192) cap = 8192;
-    if (cap < 256) cap = 256;
+    auto cap_for = [&](int win) {
+        const double expect = (double)win * win * rho;
+        int cap = (int)(1.1 * expect + 64.0);   // Poisson window count: +10 % is > 5 sigma at cfg4
+        cap = (cap + 127) & ~127;
+        if (cap > 8192) cap = 8192;
+        if (cap < 256) cap = 256;
+        return cap;
+    };
+    int cap = cap_for(plan->win);
     plan->cap = cap;
     if (plan->G == 1) {   // float2 coordinates + u8 label code per staged point
-        plan->smem = (size_t)cap * 9 + (size_t)plan->win * (plan->win + 1) * 4 + (size_t)plan->win * 4 +
-                     (size_t)(plan->win + 1) * 4 + 64;
-        if (k > tt_list_kmax()) plan->smem += (size_t)SB_NB * TT_THREADS;   // bucket select: byte histograms
+        const bool select = k > tt_list_kmax();
+        auto smem_for = [&](int win, int cap_) {
+            size_t b = (size_t)cap_ * 9 + (size_t)win * (win + 1) * 4 + (size_t)win * 4 + (size_t)(win + 1) * 4 + 64;
+            // bucket select: per-lane row tables + byte histograms
+            if (select) b += (size_t)SB_ROWS * TT_THREADS * 4 + (size_t)SB_NB * TT_THREADS;
+            return b;
+        };
+        plan->smem = smem_for(plan->win, cap);
+        if (select) {
+            // three CTAs per SM (the kernel's register budget): shrink the tile
+            // until three windows fit in the SM's 227 KB (1 KB reserved per CTA)
+            const size_t fit3 = (227 * 1024) / 3 - 1024 - 3200;   // static shared: order, phase-A words
+            int T3 = plan->T;
+            while (smem_for(T3 + 2 * A, cap_for(T3 + 2 * A)) > fit3 && T3 > (int)knob("GHN_SB_TMIN", 14)) --T3;
+            if (T3 != plan->T && smem_for(T3 + 2 * A, cap_for(T3 + 2 * A)) <= fit3) {
+                plan->T = T3;
+                plan->nt0 = (int32_t)((ix->ext[0] + T3 - 1) / T3);
+                plan->nt1 = (int32_t)((ix->ext[1] + T3 - 1) / T3);
+                plan->ntiles = (int64_t)plan->nt0 * plan->nt1;
+                plan->win = T3 + 2 * A;
+                plan->cap = cap = cap_for(plan->win);
+                plan->smem = smem_for(plan->win, cap);
+            }
+        }
         return plan->smem <= 200 * 1024;
     }
     // the warp kernel also stages each point's index (int32) and label code (u8)
@@ -1286,7 +1311,7 @@ int32_t tile2d_run(const ghn_index_view *ix, const Tile2dPlan *plan, const void 
         const int v = k > tt_list_kmax() ? 0 : lk + 1;
         ki = 4 + 2 * v + (stats ? 1 : 0);
         static const void *const thr_fns[14] = {
-            (const void *)tile2d_thr_kernel<0, false>,  (const void *)tile2d_thr_kernel<0, true>,
+            (const void *)tile2d_sel_kernel<false>,     (const void *)tile2d_sel_kernel<true>,
             (const void *)tile2d_thr_kernel<1, false>,  (const void *)tile2d_thr_kernel<1, true>,
             (const void *)tile2d_thr_kernel<2, false>,  (const void *)tile2d_thr_kernel<2, true>,
             (const void *)tile2d_thr_kernel<4, false>,  (const void *)tile2d_thr_kernel<4, true>,

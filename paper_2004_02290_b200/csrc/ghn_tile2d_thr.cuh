@@ -379,16 +379,33 @@ __device__ __forceinline__ void thr_rect_slots(const ThrWin &w, int lr, int lc, 
 }
 
 // Lock-step rounds cost the warp's LARGEST candidate count, so the tile's
-// queries are first ordered by their predicted count (the block the first
-// select walks): warps then hold queries of similar work.  The prediction
-// repeats phase A without side effects; a counting sort over the count (0..
-// 255, larger clamped) orders up to TT_SORT queries in shared memory.
-constexpr int TT_SORT = 1024;
+// queries are first ordered by their candidate count (the block the first
+// select walks): warps then hold queries of similar work.  The ordering
+// pass also does phase A of the select once per query (sel_prep) and leaves
+// its result in shared memory for the lane that takes the query.
+constexpr int TT_SORT = 1024;     // queries per chunk of the list rounds
+constexpr int SB_SORT_N = 512;   // queries ordered per chunk (a tile holds ~256)
 
-template <bool SEL>
-__device__ __forceinline__ int thr_work_key(const T2Args &a, const ThrWin &w, int qq, int t0, int t1, int r_lo,
-                                            int c_lo) {
-    const int32_t qi = a.qorder[qq];
+// Points of block(l) in the window (rows lr -+ l, columns lc -+ l, clipped).
+__device__ __forceinline__ int sel_block_count(const ThrWin &w, int lr, int lc, int l) {
+    const int c0 = max(lc - l, 0), c1 = min(lc + l, w.W - 1);
+    int n = 0;
+    for (int row = max(lr - l, 0); row <= min(lr + l, w.R - 1); ++row) {
+        const int32_t *rp = w.loc + row * w.W1;
+        n += rp[c1 + 1] - rp[c0];
+    }
+    return n;
+}
+
+// Phase A of the bucket select for one query: l* = the first layer whose
+// block holds k points (explore.py: every earlier layer leaves the buffer
+// short, so it `changed` and no stop rule applies -- T_l* = top-k of
+// block(l*)), and the skip-ahead decision (run_rounds_sel).  Packed:
+// candidates | l* << 14 | skip << 17 | live << 18; 0 = the query leaves the
+// tile path (centre outside the grid, or l* beyond the apron).
+constexpr uint32_t SEL_LIVE = 1u << 18, SEL_SKIP = 1u << 17;
+__device__ __forceinline__ uint32_t sel_prep(const T2Args &a, const ThrWin &w, int32_t qi, int t0, int t1, int r_lo,
+                                             int c_lo) {
     double q0, q1;
     if (a.q_dtype == GHN_F32) {
         const float2 qf = ((const float2 *)a.Q)[qi];
@@ -401,68 +418,63 @@ __device__ __forceinline__ int thr_work_key(const T2Args &a, const ThrWin &w, in
     const int64_t cc0 = cell_id(q0, a.w0, a.inv0, a.pow2 & 1u) - a.lo0;
     const int64_t cc1 = cell_id(q1, a.w1, a.inv1, (a.pow2 >> 1) & 1u) - a.lo1;
     const int64_t tr0 = (int64_t)t0 * a.T, tc0 = (int64_t)t1 * a.T;
-    if (cc0 < tr0 || cc0 >= tr0 + a.T || cc1 < tc0 || cc1 >= tc0 + a.T || cc0 >= a.ext0 || cc1 >= a.ext1) return 0;
+    if (cc0 < tr0 || cc0 >= tr0 + a.T || cc1 < tc0 || cc1 >= tc0 + a.T || cc0 >= a.ext0 || cc1 >= a.ext1) return 0u;
     const int lr = (int)(cc0 - r_lo), lc = (int)(cc1 - c_lo);
     const int lmax = max(max((int)cc0, a.ext0 - 1 - (int)cc0), max((int)cc1, a.ext1 - 1 - (int)cc1));
     int l = 0, cnt = 0;
     for (;; ++l) {
-        if (l > a.A) return 0;
-        if (l == 0) {
-            int s0, e0;
-            thr_rect_slots(w, lr, lc, 0, 0, 0, s0, e0);
-            cnt = e0 - s0;
-        } else {
-            for (int r = 0; r < 4 * l; ++r) {
-                int ra, rb, ca, cb, s0, e0;
-                thr_shell_rect(l, r, ra, rb, ca, cb);
-                thr_rect_slots(w, lr, lc, ra, ca, cb, s0, e0);
-                cnt += e0 - s0;
-            }
-        }
+        if (l > a.A) return 0u;
+        cnt = sel_block_count(w, lr, lc, l);
         if (cnt >= a.k || l >= lmax) break;
     }
-    if (SEL && a.mode == GHN_MODE_HEURISTIC && l < lmax && l + 1 <= a.A) {   // run_rounds_sel's skip-ahead
+    // Skip-ahead (heuristic mode, fp32 queries): when block(l*) is barely
+    // full (expected k-th radius beyond 0.8 of the block's half-width)
+    // shell(l*+1) will most likely change the top-k, so the select runs over
+    // block(l*+1) at once and learns changed(l*+1) from its members.
+    uint32_t skip = 0u;
+    if (a.mode == GHN_MODE_HEURISTIC && a.q_dtype == GHN_F32 && l < lmax && l + 1 <= a.A && cnt > 0) {
         const double kc = (double)a.k * (2.0 * l + 1.0) * (2.0 * l + 1.0) / (3.14159265358979 * (double)cnt);
         const double fc = 0.8 * ((double)l + 0.5);
         if (kc > fc * fc) {
-            int sc = 0;
-            for (int r = 0; r < 4 * (l + 1); ++r) {
-                int ra, rb, ca, cb, s0, e0;
-                thr_shell_rect(l + 1, r, ra, rb, ca, cb);
-                thr_rect_slots(w, lr, lc, ra, ca, cb, s0, e0);
-                sc += e0 - s0;
+            const int c2 = sel_block_count(w, lr, lc, l + 1);
+            if (c2 <= a.sb_capn) {
+                skip = SEL_SKIP;
+                cnt = c2;
             }
-            if (cnt + sc <= a.sb_capn) cnt += sc;
         }
     }
-    return min(cnt, 255);
+    return (uint32_t)cnt | ((uint32_t)l << 14) | skip | SEL_LIVE;
 }
 
-// ord[0, c1 - c0) = the local indices of queries [c0, c1) sorted by work key.
-template <bool SEL>
-__device__ __forceinline__ void thr_sort_chunk(const T2Args &a, const ThrWin &w, int c0, int c1, int t0, int t1,
-                                               int r_lo, int c_lo, int *hcnt, uint16_t *kr, uint16_t *ord) {
-    for (int i = threadIdx.x; i < 256; i += TT_THREADS) hcnt[i] = 0;
+// info[i] = sel_prep of query c0 + i; ord[0, c1 - c0) = the local indices
+// sorted by (skip-ahead, candidate count 0..255, larger clamped): a counting sort.
+__device__ __forceinline__ void sel_sort_chunk(const T2Args &a, const ThrWin &w, int c0, int c1, int t0, int t1,
+                                               int r_lo, int c_lo, int *hcnt, uint16_t *kr, uint16_t *ord,
+                                               uint32_t *info) {
+    for (int i = threadIdx.x; i < 512; i += TT_THREADS) hcnt[i] = 0;
     __syncthreads();
     for (int i = threadIdx.x; i < c1 - c0; i += TT_THREADS) {
-        const int key = thr_work_key<SEL>(a, w, c0 + i, t0, t1, r_lo, c_lo);
+        const uint32_t f = sel_prep(a, w, a.qorder[c0 + i], t0, t1, r_lo, c_lo);
+        info[i] = f;
+        // skip-ahead queries together (their pass 2 also tracks the shell), then by count
+        const int key = a.sb_sort ? min((int)(f & 0x3fffu), 255) + ((f & SEL_SKIP) ? 256 : 0) : 0;
         const int rank = atomicAdd(&hcnt[key], 1);
         kr[2 * i] = (uint16_t)key;
         kr[2 * i + 1] = (uint16_t)rank;
     }
     __syncthreads();
-    if (threadIdx.x < 32) {   // exclusive scan of the 256 counters, 8 per lane
-        int v[8], sum = 0;
+    if (threadIdx.x < 32) {   // exclusive scan of the 512 counters, 16 per lane
+        int v[16], sum = 0;
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            v[j] = hcnt[threadIdx.x * 8 + j];
+        for (int j = 0; j < 16; ++j) {
+            v[j] = hcnt[threadIdx.x * 16 + j];
             sum += v[j];
         }
         const int incl = warp_inclusive_scan(sum);
         int run = incl - sum;
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            hcnt[threadIdx.x * 8 + j] = run;
+        for (int j = 0; j < 16; ++j) {
+            hcnt[threadIdx.x * 16 + j] = run;
             run += v[j];
         }
     }
@@ -767,70 +779,217 @@ __device__ __forceinline__ void run_rounds_thr(const T2Args &a, const ThrWin &w,
 
 // ---------------------------------------------------------------- k > 32
 // Bucket select (k in (32, 255]): the bubble's cost grows with k, so for
-// large k block(l*) is passed over twice in lock-step.  Pass 1 histograms
-// the packed keys (pass 1 from fp32 keys: the same bucket edges) into SB_NB
-// buckets of 2^-SB_MB octave (packed >> SB_S: exponent and SB_MB mantissa
-// bits -- bucket edges are d-part edges) around the expected k-th key, in a
-// per-lane byte histogram in shared memory; the bucket bb where the count
-// reaches k follows.  Pass 2 (exact keys) votes every candidate below bb and
-// bubbles the bucket-bb candidates into a list of SB_C + 1: the k-th is its
-// r-th entry (r = k - exact count below bb).  Later shells are checked
-// compare-only; a shell that changes the top-k makes its block the next
-// select (for >= SB_REDO lanes of the warp; a lone one goes to the generic
-// kernel), as does a boundary bucket holding the k-th beyond SB_C.  Pass 1's
-// counts are approximate (fp32 keys near an edge, byte counters that wrap
-// beyond 255): pass 2's exact counts must still put the k-th in bb.
+// large k block(l*) is passed over twice in lock-step, one candidate per lane
+// per step, on fp32 keys; only the few candidates around the k-th get the
+// exact fp64 key (numpy einsum order).
+//   Pass 1 histograms fp32 keys into SB_NB buckets of 2^-SB_MB octave
+//     (exponent and SB_MB mantissa bits -- bucket edges are d-part edges)
+//     around the expected k-th key, in a per-lane byte histogram in shared
+//     memory; the bucket bb where the count reaches k follows.
+//   Pass 2 classifies every candidate by its fp32 key again: more than
+//     `ulps` below bucket bb's lower edge it is a member (voted at once: one
+//     shift and one add), more than `ulps` above the upper edge it is not,
+//     and the candidates in between (bucket bb itself: ~1 % of them) have
+//     their slot noted in the lane's (now free) histogram words.
+//   The noted candidates are then re-keyed exactly, in lock-step over the
+//     warp's largest count: below bb's lower edge (a d-part edge) they are
+//     members, the others are bubbled into a list of SB_C + 1 -- the k-th is
+//     its r-th entry (r = k - members below) and must lie inside bucket bb.
+// The fp32 key (two subtractions, a product and an fma of fp32 values) is
+// within 5 ulps of the exact one for fp32 queries, so both sure classes are
+// exact with ulps = 8; for fp64 queries the fp32 key uses the rounded query
+// and ulps grows with |q| / sqrt(key) (sel_ulps).  Pass 1 only proposes bb:
+// every count that decides the result is taken from pass 2 and the exact
+// re-keying.
+// Both passes walk the block through a per-lane table of its non-empty rows
+// (slot ranges, filled once per select) with a branch-free advance: the
+// per-lane row changes cost no divergent code.
+// Later shells are checked compare-only; a shell that changes the top-k makes
+// its block the next select (for >= SB_REDO lanes of the warp; a lone one
+// goes to the generic kernel), as does a boundary bucket holding the k-th
+// beyond SB_C.
 constexpr int SB_NB = 64;   // buckets (0 and SB_NB-1 catch the tails)
 #ifndef SB_MB
 #define SB_MB 5             // mantissa bits in a bucket index: 2^SB_MB buckets per octave (4: -2 %)
 #endif
 constexpr int SB_S = 21 - SB_MB;   // packed >> SB_S: exponent + SB_MB mantissa bits
 constexpr int SB_C = 8;     // boundary list capacity
-constexpr int SB_REDO = 8;  // fewest lanes of a warp re-selecting over a larger block
+constexpr int SB_LMAX = 4;  // largest block half-width the row table holds
+constexpr int SB_ROWS = 2 * SB_LMAX + 2;   // table words per lane: the rows + the closing sentinel
+constexpr int SB_F32_S = 23 - SB_MB;       // fp32 bits >> SB_F32_S: exponent + SB_MB mantissa bits
+constexpr int SB_F32_SHIFT = (1023 - 127) << SB_MB;   // fp64 bucket index = fp32 bucket index + this
+constexpr int SB_NOTE = SB_NB / 4;         // candidates a lane can note for exact re-keying (one per histogram word)
+constexpr uint32_t SB_SENT = 0xffff0000u;  // table sentinel: slots [0, 65535) -- never exhausted
 
-__device__ __forceinline__ int sb_bucket(uint32_t pk, int bbase) {
-    return min(max((int)(pk >> SB_S) - bbase, 0), SB_NB - 1);
+// min(max(x, 0), hi) in one instruction (VIMNMX.RELU)
+__device__ __forceinline__ int sb_clamp(int x, int hi) {
+    int r;
+    asm("min.relu.s32 %0, %1, %2;" : "=r"(r) : "r"(x), "r"(hi));
+    return r;
 }
 
-// The same bucket from an fp32 key (fp32 queries): bucket edges are the same
-// reals (exponent + 4 mantissa bits; the fp64 index = fp32 index + (1023 -
-// 127) * 16).  The fp32 key is within a few ulps of the exact key, so the
-// bucket is exact unless the key lies within 8 ulps of an edge (`edge`).
-constexpr int SB_F32_SHIFT = (1023 - 127) << SB_MB;
-__device__ __forceinline__ int sb_bucket32(float2 c, float q0f, float q1f, int bbase, bool &edge) {
-    const float dx = c.x - q0f, dy = c.y - q1f;
-    const uint32_t bits = __float_as_uint(__fmaf_rn(dy, dy, dx * dx));
-    constexpr uint32_t M = (1u << (23 - SB_MB)) - 1u;
-    edge = ((bits + 8u) & M) < 16u;
-    return min(max((int)(bits >> (23 - SB_MB)) + SB_F32_SHIFT - bbase, 0), SB_NB - 1);
+// fp32 key bits of a staged point (identical in both passes)
+__device__ __forceinline__ uint32_t sb_bits32(float dx, float dy) {
+    return __float_as_uint(__fmaf_rn(dy, dy, __fmul_rn(dx, dx)));
 }
 
-template <bool STATS>
-__device__ __forceinline__ void run_rounds_sel(const T2Args &a, const ThrWin &w, uint32_t *hist, const uint16_t *ord, int *s_grp, int qb, int qe,
+// The hot loops address shared memory through 32-bit shared-space addresses
+// (generic pointers cost 64-bit arithmetic per step).
+__device__ __forceinline__ uint32_t sm_addr(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+    return v;
+}
+__device__ __forceinline__ uint32_t lds_u8(uint32_t addr) {
+    uint32_t v;
+    asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(addr));
+    return v;
+}
+__device__ __forceinline__ float2 lds_f2(uint32_t addr) {
+    float2 v;
+    asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(addr));
+    return v;
+}
+
+// Lock-step walk over a lane's row table (word j at tab[j * TT_THREADS] =
+// first slot | end slot << 16 of its j-th non-empty row, closed by SB_SENT).
+// Every lane consumes slot p each step; a lane whose row is exhausted moves
+// to the prefetched next row (selects only).  A lane past its last row -- or
+// an idle one -- walks the sentinel's slots 0, 1, ... (in bounds: steps <=
+// staged points); the caller masks what it computes there.
+struct SelWalk {
+    uint32_t tp;   // shared address of the prefetched word
+    uint32_t nx;
+    int p, e;
+    __device__ __forceinline__ void start(uint32_t tab, bool on) {
+        const uint32_t w0 = on ? lds_u32(tab) : SB_SENT;
+        p = (int)(w0 & 0xffffu);
+        e = (int)(w0 >> 16);
+        tp = tab + TT_THREADS * 4;
+        nx = lds_u32(tp);
+    }
+    __device__ __forceinline__ void step() {
+        p += 1;
+        const bool adv = p >= e;
+        p = adv ? (int)(nx & 0xffffu) : p;
+        e = adv ? (int)(nx >> 16) : e;
+        tp += adv ? TT_THREADS * 4 : 0;
+        nx = lds_u32(tp);
+    }
+};
+
+template <bool WIDE> struct SelCnt { typedef uint32_t type; };
+template <> struct SelCnt<true> { typedef uint64_t type; };
+
+__device__ __forceinline__ int sel_bytesum(uint32_t v) { return (int)__dp4a(v, 0x01010101u, 0u); }
+__device__ __forceinline__ int sel_bytesum(uint64_t v) {
+    return (int)__dp4a((uint32_t)v, 0x01010101u, __dp4a((uint32_t)(v >> 32), 0x01010101u, 0u));
+}
+
+// Skip-ahead lanes: is a candidate of block(ls) in shell(ls)?  From fp32
+// coordinates: u = the candidate's Chebyshev distance from the centre of q's
+// cell in units of block(ls-1)'s half-width; u > 1 + eps: surely in the
+// shell, u < 1 - eps: surely inside block(ls-1), else undecided (the query
+// leaves the tile path if such a candidate is a member).  Other lanes carry
+// s = 0: u = 0, always inside.
+struct SelGeo {
+    float s0, s1, o0, o1;
+    __device__ __forceinline__ float u(float dx, float dy) const {
+        return fmaxf(fabsf(__fmaf_rn(dx, s0, o0)), fabsf(__fmaf_rn(dy, s1, o1)));
+    }
+};
+constexpr float SEL_GEO_LO = 1.0f - 2e-5f, SEL_GEO_HI = 1.0f + 2e-5f;
+
+// Pass 2 for the whole warp.  Sure members are voted into cn; the slots of
+// the candidates to re-key are noted at note[j * TT_THREADS] (low half).
+// SKIP: geo counts the sure members beyond SEL_GEO_LO (low half) and beyond
+// SEL_GEO_HI (high half).
+template <bool SKIP, bool WIDE>
+__device__ __forceinline__ void sel_pass2(uint32_t xy_s, uint32_t sl_s, uint32_t myr_s, uint32_t note_s, bool sel, int n,
+                                          int steps, float q0f, float q1f, uint32_t tlo, uint32_t span,
+                                          const SelGeo &g, typename SelCnt<WIDE>::type &cn_out, int &noted,
+                                          uint32_t &geo_out) {
+    typedef typename SelCnt<WIDE>::type cnt_t;
+    cnt_t cn = 0;
+    uint32_t geo = 0u;
+    uint32_t np = note_s;
+    SelWalk wk;
+    wk.start(myr_s, sel);
+    const int n2 = sel ? n : 0;
+    for (int it = 0; it < steps; ++it) {
+        const float2 c = lds_f2(xy_s + 8u * (uint32_t)wk.p);
+        const uint32_t lab8 = lds_u8(sl_s + (uint32_t)wk.p);   // label code * 8
+        const float dx = __fsub_rn(c.x, q0f), dy = __fsub_rn(c.y, q1f);
+        const uint32_t bits = sb_bits32(dx, dy);
+        const bool have = it < n2;
+        const bool low = have && bits < tlo;
+        const bool amb = have && (uint32_t)(bits - tlo) < span;
+        if (WIDE) {
+            const uint64_t inc = 1ull << lab8;
+            cn += low ? (cnt_t)inc : (cnt_t)0;
+        } else {
+            const uint32_t inc = __funnelshift_l(0u, 1u, lab8);   // 1 << lab8, lab8 <= 24
+            cn += low ? (cnt_t)inc : (cnt_t)0;
+        }
+        if (SKIP) {
+            const float u = g.u(dx, dy);
+            geo += low && u > SEL_GEO_LO ? 1u : 0u;
+            geo += low && u > SEL_GEO_HI ? 0x10000u : 0u;
+        }
+        if (amb) asm volatile("st.shared.u16 [%0], %1;" ::"r"(np), "h"((uint16_t)wk.p) : "memory");
+        np += amb ? TT_THREADS * 4 : 0;
+        wk.step();
+    }
+    cn_out = cn;
+    noted = (int)((np - note_s) / (TT_THREADS * 4));
+    geo_out = geo;
+}
+
+// fp32 key bits this far from an edge of bucket bb may be on the other side
+// in exact arithmetic.  fp32 queries: the fp32 key is within 5 ulps.  fp64
+// queries: the fp32 key is computed from the rounded query, off by at most
+// |q| 2^-24 per axis, i.e. 2^-23 (|q0| + |q1|) / sqrt(key) relative -- a
+// multiple of the fp32 ulp (2^-23 .. 2^-24 relative) taken at the bucket's
+// lower edge, doubled.  0 = the bucket cannot be classified in fp32.
+__device__ __forceinline__ uint32_t sel_ulps(bool f32q, double q0, double q1, double edge_lo) {
+    if (f32q) return 8u;
+    if (!(edge_lo > 0.0)) return 0u;
+    const double m = 4.0 * (fabs(q0) + fabs(q1)) * rsqrt(edge_lo) + 8.0;
+    return m < (double)(1u << (SB_F32_S - 2)) ? (uint32_t)m : 0u;
+}
+
+template <bool STATS, bool WIDE>
+__device__ __forceinline__ void run_rounds_sel(const T2Args &a, const ThrWin &w, uint32_t *hist, uint32_t *rtab,
+                                               const uint16_t *ord, const uint32_t *info, int *s_grp, int qb, int qe,
                                                int t0, int t1, int r_lo, int c_lo, ThrTotals &tot) {
+    typedef typename SelCnt<WIDE>::type cnt_t;
     const int k = a.k;
     const uint32_t lmask = (uint32_t)a.lmask;
     const uint32_t fmask = 2u * lmask + 1u;   // label bits + the shell flag above them
-    const bool f32q = a.q_dtype == GHN_F32;   // fp32 queries: fp32 keys prefilter the buckets
-    const int64_t tr0 = (int64_t)t0 * a.T, tc0 = (int64_t)t1 * a.T;
-    uint32_t *myh = hist + threadIdx.x;   // word i of this lane at myh[i * TT_THREADS]
+    const bool f32q = a.q_dtype == GHN_F32;
+    uint32_t *myh = hist + threadIdx.x;       // word i of this lane at myh[i * TT_THREADS]
+    uint32_t *myr = rtab + threadIdx.x;       // row-table word j at myr[j * TT_THREADS]
+    const uint32_t myh_s = sm_addr(myh), myr_s = sm_addr(myr), xy_s = sm_addr(w.xy), sl_s = sm_addr(w.sl);
     for (;;) {
         int g0 = 0;   // the next group of 32 (sorted) queries for this warp
         if ((threadIdx.x & 31) == 0) g0 = atomicAdd(s_grp, 32);
         g0 = __shfl_sync(GHN_FULL, g0, 0);
         if (g0 >= qe - qb) break;
-        const int qr = qb + g0 + (int)(threadIdx.x & 31);
-        bool live = qr < qe;
-        // heaviest groups first (ord is ascending in predicted work): the
+        const int qr = g0 + (int)(threadIdx.x & 31);
+        bool live = qr < qe - qb;
+        // heaviest groups first (ord is ascending in candidate count): the
         // CTA's tail is then a light group
-        const int qq = live ? qb + ord[qe - 1 - qr] : 0;
+        const int li = live ? (int)ord[qe - qb - 1 - qr] : 0;
+        const uint32_t f = live ? info[li] : 0u;
         int32_t qi = 0;
         double q0 = 0.0, q1 = 0.0;
         float q0f = 0.0f, q1f = 0.0f;
         int64_t cc0 = 0, cc1 = 0;
         int lr = 0, lc = 0, lmax = 0, l = 0, cnt = 0;
+        bool skipm = false;
         if (live) {
-            qi = a.qorder[qq];
+            qi = a.qorder[qb + li];
             if (a.q_dtype == GHN_F32) {
                 const float2 qf = ((const float2 *)a.Q)[qi];
                 q0 = (double)qf.x;
@@ -840,82 +999,59 @@ __device__ __forceinline__ void run_rounds_sel(const T2Args &a, const ThrWin &w,
             } else {
                 q0 = ((const double *)a.Q)[2 * (int64_t)qi];
                 q1 = ((const double *)a.Q)[2 * (int64_t)qi + 1];
+                q0f = (float)q0;
+                q1f = (float)q1;
             }
-            cc0 = cell_id(q0, a.w0, a.inv0, a.pow2 & 1u) - a.lo0;
-            cc1 = cell_id(q1, a.w1, a.inv1, (a.pow2 >> 1) & 1u) - a.lo1;
-            if (cc0 < tr0 || cc0 >= tr0 + a.T || cc1 < tc0 || cc1 >= tc0 + a.T || cc0 >= a.ext0 ||
-                cc1 >= a.ext1) {
+            if (!(f & SEL_LIVE)) {   // centre outside the grid / l* beyond the apron (sel_prep)
                 { FB_REASON(1); push_fallback(a, qi); }
                 live = false;
             }
         }
         if (live) {
+            cc0 = cell_id(q0, a.w0, a.inv0, a.pow2 & 1u) - a.lo0;
+            cc1 = cell_id(q1, a.w1, a.inv1, (a.pow2 >> 1) & 1u) - a.lo1;
             lr = (int)(cc0 - r_lo);
             lc = (int)(cc1 - c_lo);
             lmax = max(max((int)cc0, a.ext0 - 1 - (int)cc0), max((int)cc1, a.ext1 - 1 - (int)cc1));
-            for (;;) {
-                if (l > a.A) {
-                    { FB_REASON(2); push_fallback(a, qi); }
-                    live = false;
-                    break;
-                }
-                if (l == 0) {
-                    int s, e;
-                    thr_rect_slots(w, lr, lc, 0, 0, 0, s, e);
-                    cnt = e - s;
-                } else {
-                    for (int r = 0; r < 4 * l; ++r) {
-                        int ra, rb, ca, cb, s, e;
-                        thr_shell_rect(l, r, ra, rb, ca, cb);
-                        thr_rect_slots(w, lr, lc, ra, ca, cb, s, e);
-                        cnt += e - s;
-                    }
-                }
-                if (cnt >= k || l >= lmax) break;
-                ++l;
-            }
+            l = (int)((f >> 14) & 7u);
+            cnt = (int)(f & 0x3fffu);
+            skipm = (f & SEL_SKIP) != 0u;
         }
         // Select over block(ls) (lock-step passes), then check the later
         // shells compare-only; a shell that changes the top-k makes its
         // block the next select (explore.py:104-130).
-        int ls = l, layers = l, cls = 0;
+        int ls = l + (skipm ? 1 : 0), layers = l, cls = 0;
         bool need = live, fin = false;
-        // Heuristic mode, l* barely full (expected k-th radius beyond 0.8 of
-        // the block's half-width): shell(l*+1) will most likely change the
-        // top-k, so select over block(l*+1) at once and learn changed(l*+1)
-        // from a flag on the shell's candidates (T_{l*+1} holds one of them).
-        // Only when block(l*+1) adds no lock-step steps (the warp's largest
-        // block(l*) holds at least as many points).
-        bool skipm = false;
-        const int wmax = __reduce_max_sync(GHN_FULL, live ? cnt : 0);
-        if (live && a.mode == GHN_MODE_HEURISTIC && l < lmax && l + 1 <= a.A) {
-            const double kc = (double)k * (2.0 * l + 1.0) * (2.0 * l + 1.0) / (3.14159265358979 * (double)cnt);
-            const double fc = 0.8 * ((double)l + 0.5);
-            if (kc > fc * fc) {
-                int sc = 0;
-                for (int r = 0; r < 4 * (l + 1); ++r) {
-                    int ra, rb, ca, cb, s0, e0;
-                    thr_shell_rect(l + 1, r, ra, rb, ca, cb);
-                    thr_rect_slots(w, lr, lc, ra, ca, cb, s0, e0);
-                    sc += e0 - s0;
-                }
-                if (cnt + sc <= (a.sb_wmax ? wmax : a.sb_capn)) {
-                    skipm = true;
-                    ls = l + 1;
-                    cnt += sc;
-                }
-            }
-        }
-        uint64_t cn = 0;
+        cnt_t cn = 0;
         uint32_t tau = 0, tm = 0;
         double upper = 0.0;
-        const RectBound rb0 = live ? RectBound(a, q0, q1, cc0, cc1) : RectBound();
         while (__any_sync(GHN_FULL, need)) {
+            if (need && ls > SB_LMAX) {   // beyond the row table
+                { FB_REASON(2); push_fallback(a, qi); }
+                need = false;
+            }
+            // ---- the block's non-empty rows -> this lane's table
+            {
+                const int nrows = need ? 2 * ls + 1 : 0;
+                const int rmax = __reduce_max_sync(GHN_FULL, nrows);
+                int jw = 0, tot_n = 0;
+                for (int j = 0; j < rmax; ++j) {
+                    int s = 0, e = 0;
+                    if (j < nrows) thr_rect_slots(w, lr, lc, j - ls, -ls, ls, s, e);
+                    if (e > s) {
+                        myr[jw * TT_THREADS] = (uint32_t)s | ((uint32_t)e << 16);
+                        ++jw;
+                        tot_n += e - s;
+                    }
+                }
+                myr[jw * TT_THREADS] = SB_SENT;
+                if (need) cnt = tot_n;
+            }
             // expected k-th key from the block's density
             int bbase = 0;
             if (need) {
                 const double side = (double)(2 * ls + 1);
-                const double kest = (double)k * side * side * a.w0 * a.w1 / (3.14159265358979 * (double)cnt);
+                const double kest = (double)k * side * side * a.w0 * a.w1 / (3.14159265358979 * (double)max(cnt, 1));
                 // the 62 inner buckets span 62 / 2^SB_MB octaves centred on kest
                 const double klo = kest * exp2(-0.5 * (SB_NB - 2) / (double)(1 << SB_MB));
                 const uint32_t top = __funnelshift_l((uint32_t)__double2loint(klo), (uint32_t)__double2hiint(klo), 1);
@@ -925,120 +1061,161 @@ __device__ __forceinline__ void run_rounds_sel(const T2Args &a, const ThrWin &w,
             for (int i = 0; i < SB_NB / 4; ++i) myh[i * TT_THREADS] = 0u;
             const int n = need ? cnt : 0;
             const int steps = __reduce_max_sync(GHN_FULL, n);
-            // ---- pass 1: histogram
+            // ---- pass 1: histogram of fp32 keys (bucket b: byte b & 3 of word
+            // b >> 2).  Branch-free: an idle lane adds 0 to its own word.
             {
-                int ra = -ls, p = 0, e = 0;
-                if (need) thr_rect_slots(w, lr, lc, ra, -ls, ls, p, e);
+                SelWalk wk;
+                wk.start(myr_s, need);
+                const int kb = SB_F32_SHIFT - bbase;
                 for (int it = 0; it < steps; ++it) {
-                    const bool have = it < n;
-                    while (have && p >= e) {
-                        ++ra;
-                        thr_rect_slots(w, lr, lc, ra, -ls, ls, p, e);
-                    }
-                    // approximate buckets are fine here: pass 2 recounts exactly.
-                    // Branch-free: an idle lane adds 0 to its own word.
-                    const int pp = have ? p : 0;
-                    bool edge;
-                    const int b = f32q ? sb_bucket32(w.xy[pp], q0f, q1f, bbase, edge)
-                                       : sb_bucket(thr_pack(w.xy[pp], q0, q1, 0u, fmask), bbase);
-                    atomicAdd(&myh[(b >> 2) * TT_THREADS], have ? 1u << (8 * (b & 3)) : 0u);   // one RED, private word
-                    p += have ? 1 : 0;
+                    const float2 c = lds_f2(xy_s + 8u * (uint32_t)wk.p);
+                    const uint32_t bits = sb_bits32(__fsub_rn(c.x, q0f), __fsub_rn(c.y, q1f));
+                    const int b = sb_clamp((int)(bits >> SB_F32_S) + kb, SB_NB - 1);
+                    const uint32_t inc = it < n ? __funnelshift_l(0u, 1u, (uint32_t)b << 3) : 0u;
+                    asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(myh_s + (((uint32_t)b & 0x3cu) << 8)), "r"(inc)
+                                 : "memory");
+                    wk.step();
                 }
             }
-            int bb = 0, below = 0, nbb = 0;
+            int bb = 0;
             bool sel = need;
-            if (sel) {   // the bucket where the running count reaches k
-                int cum = 0;
-                bool found = false;
-                for (int i = 0; i < SB_NB / 4 && !found; ++i) {
-                    const uint32_t wd = myh[i * TT_THREADS];
+            {   // the bucket where the running count reaches k (all lanes, unrolled: no divergence)
+                int cum = 0, cums = 0, wi = -1;
+                uint32_t ws = 0u, wprev = 0u, wnext = 0u, last = 0u;
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) {
-                        const int c = (int)((wd >> (8 * j)) & 0xffu);
-                        if (!found && cum + c >= k) {
-                            bb = 4 * i + j;
-                            below = cum;
-                            nbb = c;
-                            found = true;
-                        }
-                        cum += c;
-                    }
+                for (int i = 0; i < SB_NB / 4; ++i) {
+                    const uint32_t wd = myh[i * TT_THREADS];
+                    const int sum = sel_bytesum(wd);
+                    const bool hit = wi < 0 && cum + sum >= k;
+                    wnext = wi == i - 1 && i > 0 ? wd : wnext;
+                    wprev = hit ? last : wprev;
+                    wi = hit ? i : wi;
+                    ws = hit ? wd : ws;
+                    cums = hit ? cum : cums;
+                    cum += sum;
+                    last = wd;
                 }
                 // more than 255 candidates: a byte counter may have carried
                 // into its neighbour (or out of the word); each carry loses
                 // >= 255 from the decoded total, so the total is exact iff none did
-                bool wrap = false;
-                if (n > 255) {
-                    int tot = 0;
-                    for (int i = 0; i < SB_NB / 4; ++i) {
-                        const uint32_t wd = myh[i * TT_THREADS];
-                        tot += (int)((wd & 0xffu) + ((wd >> 8) & 0xffu) + ((wd >> 16) & 0xffu) + (wd >> 24));
-                    }
-                    wrap = tot != n;
+                const bool wrap = n > 255 && cum != n;
+                int j = 0;
+#pragma unroll
+                for (int u = 0; u < 3; ++u) {
+                    const int c = (int)((ws >> (8 * u)) & 0xffu);
+                    const bool past = j == u && cums + c < k;
+                    cums += past ? c : 0;
+                    j += past ? 1 : 0;
                 }
-                if (!found || wrap || k - below > SB_C) {   // wrapped counts, or the k-th too deep in its bucket
+                bb = 4 * max(wi, 0) + j;
+                // candidates pass 2 may note: buckets bb - 1, bb, bb + 1 (the
+                // margin reaches into the neighbours)
+                const uint64_t w3 = ((uint64_t)wnext << 40) | ((uint64_t)ws << 8) | (uint64_t)(wprev >> 24);
+                const uint32_t near3 = (uint32_t)(w3 >> (8 * j)) & 0xffffffu;
+                const int nnear = sel_bytesum(near3);
+                // wrapped counts, the k-th too deep in its bucket, or too many to note
+                if (sel && (wi < 0 || wrap || k - cums > SB_C || nnear > SB_NOTE)) {
                     { FB_REASON(3); push_fallback(a, qi); }
                     sel = false;
                 }
             }
-            // ---- pass 2: vote below bb, list of the bucket-bb candidates
+            // ---- pass 2: vote below bb, note the candidates around bucket bb
+            uint32_t tlo = 0u, span = 0u, plo = 0u;
+            {
+                // bucket bb holds the fp32 key bits [x0 << S, (x0 + 1) << S), fp64 d-parts from plo
+                const int x0 = bb + bbase - SB_F32_SHIFT;
+                const bool inrange = x0 > (16 << SB_MB) && x0 < (240 << SB_MB);   // normal fp32 range
+                plo = bb > 0 ? (uint32_t)(bb + bbase) << SB_S : 0u;
+                const uint32_t ulps = sel && inrange ? sel_ulps(f32q, q0, q1, thr_lower(plo)) : 0u;
+                const uint32_t lo_edge = bb > 0 ? ((uint32_t)x0 << SB_F32_S) - ulps : 0u;
+                const uint32_t hi_edge = bb < SB_NB - 1 ? ((uint32_t)(x0 + 1) << SB_F32_S) + ulps : 0xffffffffu;
+                if (sel && ulps == 0u) {   // keys outside the fp32 range / queries too far from the data
+                    { FB_REASON(10); push_fallback(a, qi); }
+                    sel = false;
+                }
+                tlo = lo_edge;
+                span = hi_edge - lo_edge;
+            }
+            // skip-ahead lanes: block(ls-1) around the centre of q's cell
+            SelGeo geo{0.0f, 0.0f, 0.0f, 0.0f};
+            if (sel && skipm) {
+                const double i0 = 1.0 / (((double)ls - 0.5) * a.w0), i1 = 1.0 / (((double)ls - 0.5) * a.w1);
+                geo.s0 = (float)i0;
+                geo.s1 = (float)i1;
+                geo.o0 = (float)((q0 - ((double)(a.lo0 + cc0) + 0.5) * a.w0) * i0);
+                geo.o1 = (float)((q1 - ((double)(a.lo1 + cc1) + 0.5) * a.w1) * i1);
+            }
+            cnt_t cnv = 0;
+            int noted = 0;
+            uint32_t geoc = 0u;
+            const bool anyskip = __any_sync(GHN_FULL, sel && skipm);
+            if (anyskip)
+                sel_pass2<true, WIDE>(xy_s, sl_s, myr_s, myh_s, sel, n, steps, q0f, q1f, tlo, span, geo, cnv, noted, geoc);
+            else
+                sel_pass2<false, WIDE>(xy_s, sl_s, myr_s, myh_s, sel, n, steps, q0f, q1f, tlo, span, geo, cnv, noted, geoc);
+            // ---- exact re-keying of the noted candidates (lock-step over the warp's largest count)
             uint32_t Lb[SB_C + 1];
 #pragma unroll
             for (int j = 0; j <= SB_C; ++j) Lb[j] = TT_INF;
-            if (sel) cn = 0;
-            bool chg = false;   // a shell(ls) candidate below the boundary bucket (skip mode)
-            int nlo = 0, neq = 0;   // recount of the histogram up to bb (byte counters may wrap)
+            cnt_t cnx = 0;
+            int nlx = 0, nlist = 0;
+            bool chg = (geoc >> 16) != 0u, geo_bad = (geoc >> 16) != (geoc & 0xffffu);
             {
-                int ra = -ls, p = 0, e = 0, pi0 = 0, pi1 = 0;
-                if (sel) {
-                    thr_rect_slots(w, lr, lc, ra, -ls, ls, p, e);
-                    thr_rect_slots(w, lr, lc, ra, -(ls - 1), ls - 1, pi0, pi1);
-                }
-                for (int it = 0; it < steps; ++it) {
-                    const bool have = sel && it < n;
-                    while (have && p >= e) {
-                        ++ra;
-                        thr_rect_slots(w, lr, lc, ra, -ls, ls, p, e);
-                        thr_rect_slots(w, lr, lc, ra, -(ls - 1), ls - 1, pi0, pi1);
+                const int nn = sel ? noted : 0;
+                const int nmax = __reduce_max_sync(GHN_FULL, nn);
+                for (int j = 0; j < nmax; ++j) {
+                    const bool on = j < nn;
+                    const int slot = on ? (int)(myh[j * TT_THREADS] & 0xffffu) : 0;
+                    const float2 c = w.xy[slot];
+                    const uint32_t lab8 = (uint32_t)w.sl[slot];
+                    bool insh = false, ingeo = false;
+                    if (anyskip) {
+                        const float u = geo.u(__fsub_rn(c.x, q0f), __fsub_rn(c.y, q1f));
+                        insh = u > SEL_GEO_HI;
+                        ingeo = u > SEL_GEO_LO && !insh;
                     }
-                    const int pp = have ? p : 0;
-                    const bool insh = skipm && (ra == -ls || ra == ls || pp < pi0 || pp >= pi1);
-                    const uint32_t lab = (uint32_t)w.sl[pp] | (insh ? lmask + 1u : 0u);
-                    const uint32_t pk = thr_pack(w.xy[pp], q0, q1, lab, fmask);
-                    const int b = sb_bucket(pk, bbase);
-                    const bool low = have && b < bb;   // branch-free vote below the boundary bucket
-                    cn += low ? 1ull << (8 * (lab & lmask)) : 0ull;
-                    chg |= low && insh;
-                    nlo += low ? 1 : 0;
-                    const bool inb = have && b == bb;
-                    neq += inb ? 1 : 0;
-                    if (__any_sync(GHN_FULL, inb)) thr_bubble(Lb, inb ? pk : TT_INF);
-                    p += have ? 1 : 0;
+                    const uint32_t pk = thr_pack(c, q0, q1, (lab8 >> 3) | (insh ? lmask + 1u : 0u), fmask);
+                    const bool lowx = on && pk < plo;
+                    const bool lst = on && !lowx;
+                    cnx += lowx ? (cnt_t)1 << lab8 : (cnt_t)0;
+                    nlx += lowx ? 1 : 0;
+                    nlist += lst ? 1 : 0;
+                    chg |= lowx && insh;
+                    geo_bad |= on && ingeo;   // (conservative: also when the candidate ends up beyond the k-th)
+                    thr_bubble(Lb, lst ? pk : TT_INF);
                 }
             }
             need = false;
             bool more = false;
             if (sel) {
-                // pass 1 counted approximately (fp32 keys, byte counters that may
-                // wrap): the exact counts of pass 2 must put the k-th in bucket bb
+                // sure members: at most the histogram's count below bb (< k <=
+                // 255), so no byte of cnv carried; the re-keyed ones join only
+                // when the total stays below k
+                const int nlo = sel_bytesum(cnv) + nlx;
                 const int r = k - nlo;
-                bool stop = false, bad = !(nlo < k && k <= nlo + neq && r <= SB_C);
+                bool stop = false, bad = !(nlo < k && r <= nlist && r <= SB_C);
+                cn = cnv + (bad ? (cnt_t)0 : cnx);
                 tau = thr_pick(Lb, max(r - 1, 0));
-                const uint32_t nx = r < neq ? thr_pick(Lb, r) : TT_INF;
+                const uint32_t nx = r < min(nlist, SB_C + 1) ? thr_pick(Lb, r) : TT_INF;
+                // the k-th must lie in bucket bb: every candidate pass 2 left
+                // out has its exact key at or beyond bb's upper edge
+                bad |= bb < SB_NB - 1 && (int)(tau >> SB_S) >= bb + bbase + 1;
                 tm = tau & ~fmask;
                 upper = thr_upper(tm, fmask);
 #pragma unroll
                 for (int j = 0; j < SB_C; ++j)
                     if (j < r) {
-                        cn += 1ull << (8 * (Lb[j] & lmask));
+                        cn += (cnt_t)1 << (8 * (Lb[j] & lmask));
                         chg |= (Lb[j] & (lmask + 1u)) != 0u;
                     }
                 l = layers = ls;
                 cls = cnt;
                 // layer ls filled / changed the buffer, or (skip mode) changed iff a shell member
                 const bool changed = !skipm || chg;
+                bad |= skipm && geo_bad;
                 skipm = false;
                 stop = !changed;
+                // the next listed candidate shares the k-th's d-part: undecidable
                 bad |= nx != TT_INF && (nx & ~fmask) == tm;
                 if (!bad && a.mode == GHN_MODE_GUARANTEED) {   // layer ls changed: only the bound may stop
                     const double b = __dmul_rn((double)l, a.min_w);
@@ -1051,12 +1228,18 @@ __device__ __forceinline__ void run_rounds_sel(const T2Args &a, const ThrWin &w,
                 else more = true;
             }
             // ---- later layers, compare-only
+            const RectBound rb0 = more ? RectBound(a, q0, q1, cc0, cc1) : RectBound();
             while (__any_sync(GHN_FULL, more)) {
+                bool act = false;
                 if (more) {
                     ++l;
-                    if (l > a.A) {
+                    // the whole shell first (one test, no data): beyond the k-th it
+                    // cannot change the top-k, wherever the apron ends
+                    act = !rb0.shell_beyond(a, l, upper);
+                    if (l > a.A && (STATS || act)) {
                         { FB_REASON(5); push_fallback(a, qi); }
                         more = false;
+                        act = false;
                     }
                 }
                 bool lt = false, eq = false;
@@ -1064,10 +1247,8 @@ __device__ __forceinline__ void run_rounds_sel(const T2Args &a, const ThrWin &w,
                 {
                     int rr = 0, p = 0, e = 0;
                     const int nr = 4 * l;
-                    // the whole shell first (one test); per range only if it may matter
-                    bool act = more && !rb0.shell_beyond(a, l, upper);
-                    if (more && !act) sc = thr_shell_count(w, lr, lc, l);
-                    for (;;) {
+                    if (STATS && more && !act) sc = thr_shell_count(w, lr, lc, l);
+                    for (;;) {   // per range only if it may matter
                         while (act && p >= e) {
                             if (rr >= nr) {
                                 act = false;
@@ -1082,7 +1263,7 @@ __device__ __forceinline__ void run_rounds_sel(const T2Args &a, const ThrWin &w,
                         }
                         if (!__any_sync(GHN_FULL, act)) break;
                         const int pp = act ? p : 0;
-                        const uint32_t pk = thr_pack(w.xy[pp], q0, q1, (uint32_t)w.sl[pp], fmask);
+                        const uint32_t pk = thr_pack(w.xy[pp], q0, q1, (uint32_t)w.sl[pp] >> 3, fmask);
                         lt |= act && pk < tm;
                         eq |= act && (uint32_t)(pk - tm) <= fmask;
                         p += act ? 1 : 0;
@@ -1159,7 +1340,7 @@ __device__ __forceinline__ void run_rounds_sel(const T2Args &a, const ThrWin &w,
                     thr_rect_slots(w, lr, lc, ra, -ls, ls, p, e);
                 }
                 const int pp = have ? p : 0;
-                const uint32_t pk = thr_pack(w.xy[pp], q0, q1, (uint32_t)w.sl[pp], fmask);
+                const uint32_t pk = thr_pack(w.xy[pp], q0, q1, (uint32_t)w.sl[pp] >> 3, fmask);
                 const bool mem = have && (pk & ~fmask) <= tm;
 #pragma unroll
                 for (int j = 0; j < 8; ++j)
@@ -1167,13 +1348,14 @@ __device__ __forceinline__ void run_rounds_sel(const T2Args &a, const ThrWin &w,
                 p += have ? 1 : 0;
             }
             if (tie) {
+                const uint64_t cn8 = cn;   // 8 label slots whatever the counter width
                 uint32_t w1 = TT_INF, w2 = TT_INF;
 #pragma unroll
                 for (int j = 0; j < 8; ++j)
-                    if ((int)((cn >> (8 * j)) & 0xffu) == top && j <= (int)lmask) w1 = min(w1, mn[j]);
+                    if ((int)((cn8 >> (8 * j)) & 0xffu) == top && j <= (int)lmask) w1 = min(w1, mn[j]);
 #pragma unroll
                 for (int j = 0; j < 8; ++j)
-                    if ((int)((cn >> (8 * j)) & 0xffu) == top && j <= (int)lmask && (uint32_t)j != (w1 & lmask))
+                    if ((int)((cn8 >> (8 * j)) & 0xffu) == top && j <= (int)lmask && (uint32_t)j != (w1 & lmask))
                         w2 = min(w2, mn[j]);
                 const int lbits = __popc(fmask);
                 if ((w2 >> lbits) - (w1 >> lbits) < 2u) {
@@ -1204,7 +1386,7 @@ __device__ __forceinline__ void run_rounds_sel(const T2Args &a, const ThrWin &w,
 }
 
 template <int KM, bool STATS>
-__global__ void __launch_bounds__(TT_THREADS) tile2d_thr_kernel(const T2Args a) {
+__device__ __forceinline__ void tile2d_thr_body(const T2Args &a) {
     extern __shared__ __align__(16) unsigned char sm[];
     __shared__ int s_P;
     const int t = blockIdx.x;
@@ -1252,7 +1434,8 @@ __global__ void __launch_bounds__(TT_THREADS) tile2d_thr_kernel(const T2Args a) 
         const int p0 = rstart[i], p1 = rstart[i + 1], d = delta[i];
         for (int p = p0 + (int)(threadIdx.x & 31); p < p1; p += 32) {
             sxy[p] = make_float2(__ldg(a.c0 + p + d), __ldg(a.c1 + p + d));
-            sl[p] = (uint8_t)__ldg(a.labels_perm + p + d);
+            // the bucket select keeps label code * 8: its vote is one shift and one add
+            sl[p] = (uint8_t)(KM == 0 ? __ldg(a.labels_perm + p + d) << 3 : __ldg(a.labels_perm + p + d));
         }
     }
     __syncthreads();
@@ -1263,20 +1446,22 @@ __global__ void __launch_bounds__(TT_THREADS) tile2d_thr_kernel(const T2Args a) 
             process_query_thr<KM, STATS>(a, w, a.qorder[qq], t0, t1, r_lo, c_lo, tot);
     } else if constexpr (KM == 0) {
         // the sort's counters and (key, rank) pairs live in the histogram area
-        // (free until the rounds start); the order itself stays beside it
-        __shared__ uint16_t s_ord[TT_SORT];
-        uint32_t *hist = (uint32_t *)(rstart + a.win + 1);
+        // (free until the rounds start); the order and the per-query phase-A
+        // words stay beside it
+        __shared__ uint16_t s_ord[SB_SORT_N];
+        __shared__ uint32_t s_info[SB_SORT_N];
         __shared__ int s_grp;
-        for (int c0 = qb; c0 < qe; c0 += TT_SORT) {
-            const int c1 = min(c0 + TT_SORT, qe);
+        // (the row tables first: the walk's prefetch may read one word past a lane's table)
+        uint32_t *rtab = (uint32_t *)(rstart + a.win + 1);
+        uint32_t *hist = rtab + SB_ROWS * TT_THREADS;
+        for (int c0 = qb; c0 < qe; c0 += SB_SORT_N) {
+            const int c1 = min(c0 + SB_SORT_N, qe);
             if (threadIdx.x == 0) s_grp = 0;
-            if (a.sb_sort) {
-                thr_sort_chunk<true>(a, w, c0, c1, t0, t1, r_lo, c_lo, (int *)hist, (uint16_t *)(hist + 256), s_ord);
-            } else {
-                for (int i = threadIdx.x; i < c1 - c0; i += TT_THREADS) s_ord[i] = (uint16_t)i;
-                __syncthreads();
-            }
-            run_rounds_sel<STATS>(a, w, hist, s_ord, &s_grp, c0, c1, t0, t1, r_lo, c_lo, tot);
+            sel_sort_chunk(a, w, c0, c1, t0, t1, r_lo, c_lo, (int *)hist, (uint16_t *)(hist + 512), s_ord, s_info);
+            if (a.lmask > 3)
+                run_rounds_sel<STATS, true>(a, w, hist, rtab, s_ord, s_info, &s_grp, c0, c1, t0, t1, r_lo, c_lo, tot);
+            else
+                run_rounds_sel<STATS, false>(a, w, hist, rtab, s_ord, s_info, &s_grp, c0, c1, t0, t1, r_lo, c_lo, tot);
             __syncthreads();
         }
     } else {
@@ -1301,6 +1486,18 @@ __global__ void __launch_bounds__(TT_THREADS) tile2d_thr_kernel(const T2Args a) 
             atomicAdd(&a.totals[3], v3);
         }
     }
+}
+
+// k <= 32 (register list): registers as ptxas chooses for 256 threads.
+template <int KM, bool STATS>
+__global__ void __launch_bounds__(TT_THREADS) tile2d_thr_kernel(const T2Args a) {
+    tile2d_thr_body<KM, STATS>(a);
+}
+
+// k > 32 (bucket select): three CTAs per SM (<= 80 registers).
+template <bool STATS>
+__global__ void __launch_bounds__(TT_THREADS, 3) tile2d_sel_kernel(const T2Args a) {
+    tile2d_thr_body<0, STATS>(a);
 }
 
 }  // namespace
