@@ -80,10 +80,11 @@ extern "C" size_t ghn_query_workspace_size(const ghn_index_view *ix, int64_t nq,
         return lk > b ? lk : b;
     }
     Tile2dPlan tp;
-    if (tile2d_plan(ix, nq, k, GHN_TASK_CLASSIFY, false, &tp)) {
-        size_t t = tile2d_workspace_bytes(&tp, nq);
-        if (t > b) b = t;
-    }
+    for (int stats = 0; stats < 2; ++stats)   // the tiling depends on whether QueryStats are requested
+        if (tile2d_plan(ix, nq, k, GHN_TASK_CLASSIFY, false, stats != 0, &tp)) {
+            size_t t = tile2d_workspace_bytes(&tp, nq);
+            if (t > b) b = t;
+        }
     return b;
 }
 
@@ -183,7 +184,8 @@ extern "C" int32_t ghn_query(const ghn_index_view *ix, const void *Q, int32_t q_
     const int ks = k <= 32 ? 1 : (k <= 64 ? 2 : (k <= 128 ? 4 : 8));
     Tile2dPlan tp;
     const bool want_nb = out->dist != nullptr || out->idx != nullptr;
-    if (mode != GHN_MODE_BRUTE && workspace && tile2d_plan(ix, nq, k, task, want_nb, &tp) &&
+    const bool want_stats = out->stats != nullptr || out->totals != nullptr;
+    if (mode != GHN_MODE_BRUTE && workspace && tile2d_plan(ix, nq, k, task, want_nb, want_stats, &tp) &&
         workspace_bytes >= tile2d_workspace_bytes(&tp, nq)) {
         int32_t *fb_list = nullptr, *fb_count = nullptr;
         rc = tile2d_run(ix, &tp, Q, q_dtype, nq, k, mode, out, a.inv_w, a.pow2, workspace, &fb_list,

@@ -1122,7 +1122,7 @@ static int tt_list_kmax() {
     return (int)knob("GHN_TT_LISTMAX", TT_LIST_KMAX);
 }
 
-bool tile2d_plan(const ghn_index_view *ix, int64_t nq, int32_t k, int32_t task, bool want_neighbors,
+bool tile2d_plan(const ghn_index_view *ix, int64_t nq, int32_t k, int32_t task, bool want_neighbors, bool want_stats,
                  Tile2dPlan *plan) {
     memset(plan, 0, sizeof(*plan));
     if (ix->layout != GHN_LAYOUT_DENSE || ix->d != 2 || ix->dtype != GHN_F32) return false;
@@ -1135,7 +1135,12 @@ bool tile2d_plan(const ghn_index_view *ix, int64_t nq, int32_t k, int32_t task, 
     if (ix->density_hint > rho) rho = ix->density_hint;
     int lf = 0;
     while (lf < 8 && (2.0 * lf + 1) * (2.0 * lf + 1) * rho < (double)k) ++lf;
-    const int A = (int)knob("GHN_TILE_A", lf + 2 > 4 ? 4 : lf + 2);
+    // apron: two layers beyond the layer that fills the buffer on average.  The
+    // bucket select without QueryStats needs one: a shell beyond the apron that
+    // provably cannot change the top-k is skipped without its data.
+    const bool thr = k <= TT_KMAX && ix->n_labels > 0 && ix->n_labels <= 8;
+    const int extra = thr && k > tt_list_kmax() && !want_stats ? 1 : 2;
+    const int A = (int)knob("GHN_TILE_A", lf + extra > 4 ? 4 : lf + extra);
     int T = (int)floor(sqrt(0.7 * T2_CAP / (rho > 1e-9 ? rho : 1e-9))) - 2 * A;
     const double Tmax = sqrt((double)ix->E / (sm_count() * 4.0));
     if (T > Tmax) T = (int)Tmax;

@@ -18,7 +18,8 @@ struct Tile2dPlan {
 
 // Whether the tiled path applies (2-D, DENSE, fp32, classify without
 // neighbour output) and its geometry for this k.
-bool tile2d_plan(const ghn_index_view *ix, int64_t nq, int32_t k, int32_t task, bool want_neighbors,
+// want_stats: QueryStats / totals are requested (the bucket select then stages one more apron layer).
+bool tile2d_plan(const ghn_index_view *ix, int64_t nq, int32_t k, int32_t task, bool want_neighbors, bool want_stats,
                  Tile2dPlan *plan);
 size_t tile2d_workspace_bytes(const Tile2dPlan *p, int64_t nq);
 // Bins the queries by tile and launches the tiled kernel; queries it cannot

@@ -1021,7 +1021,7 @@ __device__ __forceinline__ void run_rounds_sel(const T2Args &a, const ThrWin &w,
         // shells compare-only; a shell that changes the top-k makes its
         // block the next select (explore.py:104-130).
         int ls = l + (skipm ? 1 : 0), layers = l, cls = 0;
-        bool need = live, fin = false;
+        bool need = live, fin = false, noprune = false;
         cnt_t cn = 0;
         uint32_t tau = 0, tm = 0;
         double upper = 0.0;
@@ -1030,25 +1030,9 @@ __device__ __forceinline__ void run_rounds_sel(const T2Args &a, const ThrWin &w,
                 { FB_REASON(2); push_fallback(a, qi); }
                 need = false;
             }
-            // ---- the block's non-empty rows -> this lane's table
-            {
-                const int nrows = need ? 2 * ls + 1 : 0;
-                const int rmax = __reduce_max_sync(GHN_FULL, nrows);
-                int jw = 0, tot_n = 0;
-                for (int j = 0; j < rmax; ++j) {
-                    int s = 0, e = 0;
-                    if (j < nrows) thr_rect_slots(w, lr, lc, j - ls, -ls, ls, s, e);
-                    if (e > s) {
-                        myr[jw * TT_THREADS] = (uint32_t)s | ((uint32_t)e << 16);
-                        ++jw;
-                        tot_n += e - s;
-                    }
-                }
-                myr[jw * TT_THREADS] = SB_SENT;
-                if (need) cnt = tot_n;
-            }
             // expected k-th key from the block's density
             int bbase = 0;
+            double r2 = 0.0;   // pruning radius (squared); 0: the whole block
             if (need) {
                 const double side = (double)(2 * ls + 1);
                 const double kest = (double)k * side * side * a.w0 * a.w1 / (3.14159265358979 * (double)max(cnt, 1));
@@ -1056,10 +1040,49 @@ __device__ __forceinline__ void run_rounds_sel(const T2Args &a, const ThrWin &w,
                 const double klo = kest * exp2(-0.5 * (SB_NB - 2) / (double)(1 << SB_MB));
                 const uint32_t top = __funnelshift_l((uint32_t)__double2loint(klo), (uint32_t)__double2hiint(klo), 1);
                 bbase = (int)(top >> SB_S) - 1;
+                // the k-th key exceeds this with probability ~1e-6 (5 sigma of the
+                // count inside the radius); checked after the select
+                if (!noprune) r2 = kest * (1.0 + 5.0 * rsqrt((double)k));
+            }
+            // ---- the block's non-empty rows -> this lane's table.  Each row is
+            // clipped to the cells that can hold a point within sqrt(r2) of q
+            // (fp32 arithmetic with margins far above its rounding: a superset).
+            int n = 0;
+            {
+                const int nrows = need ? 2 * ls + 1 : 0;
+                const int rmax = __reduce_max_sync(GHN_FULL, nrows);
+                const bool prune = r2 > 0.0;
+                // q's distance to the faces of its own cell
+                const float w0f = (float)a.w0, w1f = (float)a.w1;
+                const float fl0 = (float)(q0 - (double)(a.lo0 + cc0) * a.w0), fh0 = w0f - fl0;
+                const float fl1 = (float)(q1 - (double)(a.lo1 + cc1) * a.w1), fh1 = w1f - fl1;
+                const float iw1 = 1.0f / w1f, r2f = (float)r2 * 1.0001f;
+                const float mg0 = 1e-4f * w0f, mg1 = 1e-4f * w1f;
+                int jw = 0;
+                for (int j = 0; j < rmax; ++j) {
+                    const int ra = j - ls;
+                    int ca = -ls, cb = ls;
+                    bool rowon = j < nrows;
+                    if (prune) {
+                        const float dy = fmaxf((ra > 0 ? fh0 + (float)(ra - 1) * w0f : (ra < 0 ? fl0 + (float)(-ra - 1) * w0f : 0.0f)) - mg0, 0.0f);
+                        const float rem = r2f - dy * dy;
+                        rowon = rowon && rem > 0.0f;
+                        const float dxm = sqrtf(fmaxf(rem, 0.0f)) * 1.0001f + mg1;
+                        cb = min(ls, max((int)floorf((dxm - fh1) * iw1) + 1, 0));
+                        ca = -min(ls, max((int)floorf((dxm - fl1) * iw1) + 1, 0));
+                    }
+                    int s = 0, e = 0;
+                    if (rowon) thr_rect_slots(w, lr, lc, ra, ca, cb, s, e);
+                    if (e > s) {
+                        myr[jw * TT_THREADS] = (uint32_t)s | ((uint32_t)e << 16);
+                        ++jw;
+                        n += e - s;
+                    }
+                }
+                myr[jw * TT_THREADS] = SB_SENT;
             }
 #pragma unroll
             for (int i = 0; i < SB_NB / 4; ++i) myh[i * TT_THREADS] = 0u;
-            const int n = need ? cnt : 0;
             const int steps = __reduce_max_sync(GHN_FULL, n);
             // ---- pass 1: histogram of fp32 keys (bucket b: byte b & 3 of word
             // b >> 2).  Branch-free: an idle lane adds 0 to its own word.
@@ -1078,7 +1101,7 @@ __device__ __forceinline__ void run_rounds_sel(const T2Args &a, const ThrWin &w,
                 }
             }
             int bb = 0;
-            bool sel = need;
+            bool sel = need, reprune = false;
             {   // the bucket where the running count reaches k (all lanes, unrolled: no divergence)
                 int cum = 0, cums = 0, wi = -1;
                 uint32_t ws = 0u, wprev = 0u, wnext = 0u, last = 0u;
@@ -1114,6 +1137,10 @@ __device__ __forceinline__ void run_rounds_sel(const T2Args &a, const ThrWin &w,
                 const uint32_t near3 = (uint32_t)(w3 >> (8 * j)) & 0xffffffu;
                 const int nnear = sel_bytesum(near3);
                 // wrapped counts, the k-th too deep in its bucket, or too many to note
+                if (sel && wi < 0 && r2 > 0.0) {   // fewer than k candidates inside the radius: the whole block next
+                    reprune = true;
+                    sel = false;
+                }
                 if (sel && (wi < 0 || wrap || k - cums > SB_C || nnear > SB_NOTE)) {
                     { FB_REASON(3); push_fallback(a, qi); }
                     sel = false;
@@ -1187,12 +1214,27 @@ __device__ __forceinline__ void run_rounds_sel(const T2Args &a, const ThrWin &w,
             }
             need = false;
             bool more = false;
+            const int nlo = sel_bytesum(cnv) + nlx;
+            const int r = k - nlo;
+            if (reprune) {
+                need = true;
+                noprune = true;
+            }
+            if (sel && r2 > 0.0) {
+                // the rows were clipped to the radius sqrt(r2): exact only when the
+                // k-th key lies inside it.  Else select again over the whole block.
+                const bool ok = nlo < k && r <= nlist && r <= SB_C;
+                const uint32_t t0k = thr_pick(Lb, max(r - 1, 0)) & ~fmask;
+                if (nlo < k && !(ok && thr_upper(t0k, fmask) < r2)) {
+                    sel = false;
+                    need = true;
+                    noprune = true;
+                }
+            }
             if (sel) {
                 // sure members: at most the histogram's count below bb (< k <=
                 // 255), so no byte of cnv carried; the re-keyed ones join only
                 // when the total stays below k
-                const int nlo = sel_bytesum(cnv) + nlx;
-                const int r = k - nlo;
                 bool stop = false, bad = !(nlo < k && r <= nlist && r <= SB_C);
                 cn = cnv + (bad ? (cnt_t)0 : cnx);
                 tau = thr_pick(Lb, max(r - 1, 0));
