@@ -899,7 +899,7 @@ struct SelGeo {
         return fmaxf(fabsf(__fmaf_rn(dx, s0, o0)), fabsf(__fmaf_rn(dy, s1, o1)));
     }
 };
-constexpr float SEL_GEO_LO = 1.0f - 2e-5f, SEL_GEO_HI = 1.0f + 2e-5f;
+constexpr float SEL_GEO_LO = 1.0f - 3e-6f, SEL_GEO_HI = 1.0f + 3e-6f;   // fp32 rounding of u: < 1e-6
 
 // Pass 2 for the whole warp.  Sure members are voted into cn; the slots of
 // the candidates to re-key are noted at note[j * TT_THREADS] (low half).
@@ -1226,6 +1226,7 @@ __device__ __forceinline__ void run_rounds_sel(const T2Args &a, const ThrWin &w,
                 const bool ok = nlo < k && r <= nlist && r <= SB_C;
                 const uint32_t t0k = thr_pick(Lb, max(r - 1, 0)) & ~fmask;
                 if (nlo < k && !(ok && thr_upper(t0k, fmask) < r2)) {
+                    FB_REASON(11);   // (a redo, not yet a fallback)
                     sel = false;
                     need = true;
                     noprune = true;
@@ -1265,6 +1266,12 @@ __device__ __forceinline__ void run_rounds_sel(const T2Args &a, const ThrWin &w,
                     if (b2 >= upper) stop = true;
                     else if (b2 > thr_lower(tm)) bad = true;
                 }
+#ifdef GHN_FB_REASONS
+                if (!(nlo < k)) FB_REASON(12);
+                else if (!(r <= nlist)) FB_REASON(13);
+                else if (!(r <= SB_C)) FB_REASON(14);
+                else if (bb < SB_NB - 1 && (int)(tau >> SB_S) >= bb + bbase + 1) FB_REASON(15);
+#endif
                 if (bad) { FB_REASON(4); push_fallback(a, qi); }
                 else if (stop || l >= lmax) fin = true;
                 else more = true;
