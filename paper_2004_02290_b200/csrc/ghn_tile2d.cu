@@ -80,6 +80,7 @@ struct T2Args {
     int32_t lmask;   // label-code mask of the thread kernel (2^LB - 1)
     int32_t sb_capn, sb_redo, sb_wmax, sb_sort, sb_recap;   // bucket-select lock-step knobs (see ghn_tile2d_thr.cuh)
     double tt_skipf;   // k = 3, 4 rounds: skip-ahead threshold (fraction of the block half-width)
+    int32_t tt_tab;    // k <= 32: table-driven rounds (run_rounds_tab)
 };
 
 struct Win {
@@ -1118,6 +1119,10 @@ __global__ void window_density_kernel(const int32_t *__restrict__ cell_start, co
 
 // Largest k answered with the register list; larger k use the bucket select
 // (GHN_TT_LISTMAX overrides, for measurements).
+static int tt_tab_on() {
+    return GHN_TT_TAB;
+}
+
 static int tt_list_kmax() {
     return (int)knob("GHN_TT_LISTMAX", TT_LIST_KMAX);
 }
@@ -1196,6 +1201,8 @@ bool tile2d_plan(const ghn_index_view *ix, int64_t nq, int32_t k, int32_t task, 
             size_t b = (size_t)cap_ * 9 + (size_t)win * (win + 1) * 4 + (size_t)win * 4 + (size_t)(win + 1) * 4 + 64;
             // bucket select: per-lane row tables + byte histograms
             if (select) b += (size_t)SB_ROWS * TT_THREADS * 4 + (size_t)SB_NB * TT_THREADS;
+            // list rounds: per-lane row tables (+ the word the walk prefetches past the sentinel)
+            else if (tt_tab_on()) b += (size_t)(2 * A + 3) * TT_THREADS * 4;
             return b;
         };
         plan->smem = smem_for(plan->win, cap);
@@ -1305,6 +1312,7 @@ int32_t tile2d_run(const ghn_index_view *ix, const Tile2dPlan *plan, const void 
     a.sb_wmax = (int)knob("GHN_SB_WMAX", 0);
     a.sb_sort = (int)knob("GHN_SB_SORT", 1);
     a.tt_skipf = knob("GHN_TT_SKIPF", 0.4);
+    a.tt_tab = tt_tab_on();
     const bool stats = out->stats != nullptr || out->totals != nullptr;
     // warp kernel: extraction select for small k (EXT), histogram select otherwise
     int ki = plan->G == 8 ? 1 : (plan->G == 16 ? 2 : (k >= 2 && k <= T2_EXT_MAXK ? 3 : 0));

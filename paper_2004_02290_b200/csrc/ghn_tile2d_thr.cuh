@@ -44,6 +44,9 @@ namespace ghn {
 namespace {
 
 constexpr int TT_THREADS = 256;
+#ifndef GHN_TT_TAB
+#define GHN_TT_TAB 1   // k <= 32: table-driven rounds (run_rounds_tab); 0: the round-1 rounds, for A/B builds
+#endif
 constexpr uint32_t TT_INF = 0xffffffffu;
 
 struct ThrWin {
@@ -405,7 +408,7 @@ __device__ __forceinline__ int sel_block_count(const ThrWin &w, int lr, int lc, 
 // tile path (centre outside the grid, or l* beyond the apron).
 constexpr uint32_t SEL_LIVE = 1u << 18, SEL_SKIP = 1u << 17;
 __device__ __forceinline__ uint32_t sel_prep(const T2Args &a, const ThrWin &w, int32_t qi, int t0, int t1, int r_lo,
-                                             int c_lo) {
+                                             int c_lo, bool allow_skip) {
     double q0, q1;
     if (a.q_dtype == GHN_F32) {
         const float2 qf = ((const float2 *)a.Q)[qi];
@@ -432,7 +435,7 @@ __device__ __forceinline__ uint32_t sel_prep(const T2Args &a, const ThrWin &w, i
     // shell(l*+1) will most likely change the top-k, so the select runs over
     // block(l*+1) at once and learns changed(l*+1) from its members.
     uint32_t skip = 0u;
-    if (a.mode == GHN_MODE_HEURISTIC && a.q_dtype == GHN_F32 && l < lmax && l + 1 <= a.A && cnt > 0) {
+    if (allow_skip && a.mode == GHN_MODE_HEURISTIC && a.q_dtype == GHN_F32 && l < lmax && l + 1 <= a.A && cnt > 0) {
         const double kc = (double)a.k * (2.0 * l + 1.0) * (2.0 * l + 1.0) / (3.14159265358979 * (double)cnt);
         const double fc = 0.8 * ((double)l + 0.5);
         if (kc > fc * fc) {
@@ -450,11 +453,11 @@ __device__ __forceinline__ uint32_t sel_prep(const T2Args &a, const ThrWin &w, i
 // sorted by (skip-ahead, candidate count 0..255, larger clamped): a counting sort.
 __device__ __forceinline__ void sel_sort_chunk(const T2Args &a, const ThrWin &w, int c0, int c1, int t0, int t1,
                                                int r_lo, int c_lo, int *hcnt, uint16_t *kr, uint16_t *ord,
-                                               uint32_t *info) {
+                                               uint32_t *info, bool allow_skip) {
     for (int i = threadIdx.x; i < 512; i += TT_THREADS) hcnt[i] = 0;
     __syncthreads();
     for (int i = threadIdx.x; i < c1 - c0; i += TT_THREADS) {
-        const uint32_t f = sel_prep(a, w, a.qorder[c0 + i], t0, t1, r_lo, c_lo);
+        const uint32_t f = sel_prep(a, w, a.qorder[c0 + i], t0, t1, r_lo, c_lo, allow_skip);
         info[i] = f;
         // skip-ahead queries together (their pass 2 also tracks the shell), then by count
         const int key = a.sb_sort ? min((int)(f & 0x3fffu), 255) + ((f & SEL_SKIP) ? 256 : 0) : 0;
@@ -1434,6 +1437,313 @@ __device__ __forceinline__ void run_rounds_sel(const T2Args &a, const ThrWin &w,
     }
 }
 
+// ---------------------------------------------------------------- k <= 32, table-driven
+// The register-list rounds on the select's machinery: phase A once per query
+// in the ordering pass (groups hold queries of similar candidate counts), the
+// candidates of block(l*) and of every later shell walked through the lane's
+// row table with the branch-free advance, and both clipped to the cells that
+// can matter: block(l*) to the expected k-th radius + 5 sigma (verified), a
+// later shell to the radius of the current k-th key (exact: a point outside
+// it cannot precede the k-th nor share its d-part).
+//  A  (per lane) the query and its phase-A word;
+//  B  (warp lock-step) block(l*) in batches of 8 candidates per lane, sorted
+//     by a network and merged into the list (k <= 2: bubbled);
+//  C  (warp lock-step) later layers while some lane continues: the clipped
+//     shell's candidates are bubbled into the list; the layer `changed` iff
+//     one of them precedes the k-th key it met (explore.py:117);
+//  D  the vote (predict.py:29-36) and the outputs.
+struct SelClip {
+    float fl0, fh0, fl1, fh1, w0f, w1f, iw1, mg0, mg1;
+    __device__ __forceinline__ SelClip(const T2Args &a, double q0, double q1, int64_t cc0, int64_t cc1) {
+        // q's distance to the faces of its own cell
+        w0f = (float)a.w0;
+        w1f = (float)a.w1;
+        fl0 = (float)(q0 - (double)(a.lo0 + cc0) * a.w0);
+        fh0 = w0f - fl0;
+        fl1 = (float)(q1 - (double)(a.lo1 + cc1) * a.w1);
+        fh1 = w1f - fl1;
+        iw1 = 1.0f / w1f;
+        mg0 = 1e-4f * w0f;
+        mg1 = 1e-4f * w1f;
+    }
+    // Columns [ca, cb] (offsets from q's cell, within -+ls) of row offset ra
+    // that can hold a point within sqrt(r2f) of q; false: none.  fp32 with
+    // margins far above its rounding (r2f is passed inflated): a superset.
+    __device__ __forceinline__ bool cols(int ra, int ls, float r2f, int &ca, int &cb) const {
+        const float dy =
+            fmaxf((ra > 0 ? fh0 + (float)(ra - 1) * w0f : (ra < 0 ? fl0 + (float)(-ra - 1) * w0f : 0.0f)) - mg0, 0.0f);
+        const float rem = r2f - dy * dy;
+        const float dxm = sqrtf(fmaxf(rem, 0.0f)) * 1.0001f + mg1;
+        cb = min(ls, max((int)fminf(floorf((dxm - fh1) * iw1), 64.0f) + 1, 0));
+        ca = -min(ls, max((int)fminf(floorf((dxm - fl1) * iw1), 64.0f) + 1, 0));
+        return rem > 0.0f;
+    }
+};
+
+// Packed key of a staged slot through shared-space addresses.
+__device__ __forceinline__ uint32_t tab_pack(uint32_t xy_s, uint32_t sl_s, int p, double q0, double q1, uint32_t lmask) {
+    return thr_pack(lds_f2(xy_s + 8u * (uint32_t)p), q0, q1, lds_u8(sl_s + (uint32_t)p), lmask);
+}
+
+template <int KM, bool STATS>
+__device__ __forceinline__ void run_rounds_tab(const T2Args &a, const ThrWin &w, uint32_t *rtab, int nrw,
+                                               const uint16_t *ord, const uint32_t *info, int *s_grp, int qb, int qe,
+                                               int r_lo, int c_lo, ThrTotals &tot) {
+    const int k = a.k;
+    const uint32_t lmask = (uint32_t)a.lmask;
+    uint32_t *myr = rtab + threadIdx.x;   // row-table word j at myr[j * TT_THREADS]
+    const uint32_t myr_s = sm_addr(myr), xy_s = sm_addr(w.xy), sl_s = sm_addr(w.sl);
+    for (;;) {
+        int g0 = 0;   // the next group of 32 (sorted) queries for this warp
+        if ((threadIdx.x & 31) == 0) g0 = atomicAdd(s_grp, 32);
+        g0 = __shfl_sync(GHN_FULL, g0, 0);
+        if (g0 >= qe - qb) break;
+        const int qr = g0 + (int)(threadIdx.x & 31);
+        bool live = qr < qe - qb;
+        const int li = live ? (int)ord[qe - qb - 1 - qr] : 0;   // heaviest groups first
+        const uint32_t f = live ? info[li] : 0u;
+        int32_t qi = 0;
+        double q0 = 0.0, q1 = 0.0;
+        int64_t cc0 = 0, cc1 = 0;
+        int lr = 0, lc = 0, lmax = 0, l = 0, cnt = 0;
+        if (live) {
+            qi = a.qorder[qb + li];
+            if (a.q_dtype == GHN_F32) {
+                const float2 qf = ((const float2 *)a.Q)[qi];
+                q0 = (double)qf.x;
+                q1 = (double)qf.y;
+            } else {
+                q0 = ((const double *)a.Q)[2 * (int64_t)qi];
+                q1 = ((const double *)a.Q)[2 * (int64_t)qi + 1];
+            }
+            if (!(f & SEL_LIVE)) {   // centre outside the grid / l* beyond the apron (sel_prep)
+                push_fallback(a, qi);
+                live = false;
+            }
+        }
+        if (live) {
+            cc0 = cell_id(q0, a.w0, a.inv0, a.pow2 & 1u) - a.lo0;
+            cc1 = cell_id(q1, a.w1, a.inv1, (a.pow2 >> 1) & 1u) - a.lo1;
+            lr = (int)(cc0 - r_lo);
+            lc = (int)(cc1 - c_lo);
+            lmax = max(max((int)cc0, a.ext0 - 1 - (int)cc0), max((int)cc1, a.ext1 - 1 - (int)cc1));
+            l = (int)((f >> 14) & 7u);
+            cnt = (int)(f & 0x3fffu);
+            if (2 * l + 2 > nrw) {   // beyond the row table
+                push_fallback(a, qi);
+                live = false;
+            }
+        }
+        const SelClip clip(a, q0, q1, cc0, cc1);
+        // ---- B: block(l) into the list, lock-step
+        uint32_t L[KM + 1];
+#pragma unroll
+        for (int j = 0; j <= KM; ++j) L[j] = TT_INF;
+        bool need = live, noprune = false;
+        while (__any_sync(GHN_FULL, need)) {
+#pragma unroll
+            for (int j = 0; j <= KM; ++j) L[j] = need ? TT_INF : L[j];   // (a lane that is done keeps its list)
+            // clip block(l), l >= 1, to the expected k-th radius + 5 sigma of the
+            // count inside it (checked below; the whole block otherwise)
+            double r2 = 0.0;
+            if (need && !noprune && l >= 1) {
+                const double side = (double)(2 * l + 1);
+                const double kest = (double)k * side * side * a.w0 * a.w1 / (3.14159265358979 * (double)max(cnt, 1));
+                r2 = kest * (1.0 + 5.0 * rsqrt((double)k));
+            }
+            int n = 0;
+            {
+                const int nrows = need ? 2 * l + 1 : 0;
+                const int rmax = __reduce_max_sync(GHN_FULL, nrows);
+                const float r2f = (float)r2 * 1.0001f;
+                int jw = 0;
+                for (int j = 0; j < rmax; ++j) {
+                    const int ra = j - l;
+                    int ca = -l, cb = l;
+                    bool rowon = j < nrows;
+                    if (r2 > 0.0) rowon = clip.cols(ra, l, r2f, ca, cb) && rowon;
+                    int s = 0, e = 0;
+                    if (rowon) thr_rect_slots(w, lr, lc, ra, ca, cb, s, e);
+                    if (e > s) {
+                        myr[jw * TT_THREADS] = (uint32_t)s | ((uint32_t)e << 16);
+                        ++jw;
+                        n += e - s;
+                    }
+                }
+                myr[jw * TT_THREADS] = SB_SENT;
+            }
+            const int steps = __reduce_max_sync(GHN_FULL, n);
+            SelWalk wk;
+            wk.start(myr_s, need);
+            // batches of 8 candidates per lane: sorted by a 19-comparator network,
+            // then merged into the list (NetMerge8: 41 comparators at k = 16)
+            for (int it = 0; it < steps; it += 8) {
+                uint32_t bt[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const uint32_t pk = tab_pack(xy_s, sl_s, wk.p, q0, q1, lmask);
+                    bt[u] = it + u < n ? pk : TT_INF;
+                    wk.step();
+                }
+                if constexpr (KM <= 2) {   // a list of 2-3: the bubble is cheaper than sort + merge
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) thr_bubble(L, bt[u]);
+                } else {
+                    net_sort8(bt);
+                    NetMerge8<KM + 1>::run(L, bt);
+                }
+            }
+            if (need && r2 > 0.0) {
+                // clipped rows: exact only when the k-th key lies inside the radius
+                const uint32_t tk = thr_pick(L, k - 1);
+                need = !(tk != TT_INF && thr_upper(tk & ~lmask, lmask) < r2);
+                noprune = true;
+            } else {
+                need = false;
+            }
+        }
+        int layers = l;
+        int64_t points = cnt;
+        // stop rules after layer l* (it filled the buffer: changed)
+        if (live && cnt >= k && a.mode == GHN_MODE_GUARANTEED) {
+            const double b = __dmul_rn((double)l, a.min_w);
+            const double b2 = __dmul_rn(b, b);
+            const uint32_t tk = thr_pick(L, k - 1) & ~lmask;
+            if (b2 >= thr_upper(tk, lmask)) {
+                lmax = l;   // stop
+            } else if (b2 > thr_lower(tk)) {
+                push_fallback(a, qi);
+                live = false;
+            }
+        }
+        bool more = live && l < lmax;   // continues with layer l + 1
+        bool fin = live && !more;       // answered after layer l
+        // ---- C: later layers
+        const RectBound rb0 = more ? RectBound(a, q0, q1, cc0, cc1) : RectBound();
+        while (__any_sync(GHN_FULL, more)) {
+            uint32_t tm = 0;
+            double upper = 0.0;
+            bool act = false;
+            if (more) {
+                ++l;
+                tm = thr_pick(L, k - 1) & ~lmask;
+                upper = thr_upper(tm, lmask);
+                // the whole shell first (one test, no data): beyond the k-th it
+                // cannot change the top-k, wherever the apron ends
+                act = !rb0.shell_beyond(a, l, upper);
+                if (l > a.A && (STATS || act)) {
+                    push_fallback(a, qi);
+                    more = false;
+                    act = false;
+                }
+            }
+            // the shell's ranges within sqrt(upper) of q -> the lane's table
+            int n = 0;
+            bool over = false;
+            {
+                const int nrows = act ? 2 * l + 1 : 0;
+                const int rmax = __reduce_max_sync(GHN_FULL, nrows);
+                const float r2f = (float)upper * 1.0001f;
+                int jw = 0;
+                for (int j = 0; j < rmax; ++j) {
+                    const int ra = j - l;
+                    int ca = -l, cb = l;
+                    const bool rowon = clip.cols(ra, l, r2f, ca, cb) && j < nrows;
+                    const bool edge = ra == -l || ra == l;
+                    // an inner row contributes its end cells only
+                    int s0 = 0, e0 = 0, s1 = 0, e1 = 0;
+                    if (rowon && (edge || ca == -l)) thr_rect_slots(w, lr, lc, ra, ca, edge ? cb : ca, s0, e0);
+                    if (rowon && !edge && cb == l) thr_rect_slots(w, lr, lc, ra, cb, cb, s1, e1);
+                    if (e0 > s0) {
+                        if (jw < nrw - 1) myr[jw * TT_THREADS] = (uint32_t)s0 | ((uint32_t)e0 << 16);
+                        ++jw;
+                        n += e0 - s0;
+                    }
+                    if (e1 > s1) {
+                        if (jw < nrw - 1) myr[jw * TT_THREADS] = (uint32_t)s1 | ((uint32_t)e1 << 16);
+                        ++jw;
+                        n += e1 - s1;
+                    }
+                }
+                over = jw > nrw - 1;
+                myr[min(jw, nrw - 1) * TT_THREADS] = SB_SENT;
+            }
+            if (over) {   // more ranges than the table holds
+                push_fallback(a, qi);
+                more = false;
+                act = false;
+                n = 0;
+            }
+            bool lt = false, eq = false;
+            {
+                const int steps = __reduce_max_sync(GHN_FULL, n);
+                SelWalk wk;
+                wk.start(myr_s, act);
+                uint32_t lk1 = thr_pick(L, k);   // a candidate at or beyond the (k+1)-th leaves L[0..k] alone
+                for (int it = 0; it < steps; ++it) {
+                    const bool have = it < n;
+                    const uint32_t pk = tab_pack(xy_s, sl_s, wk.p, q0, q1, lmask);
+                    lt |= have && pk < tm;
+                    eq |= have && (uint32_t)(pk - tm) <= lmask;
+                    const bool ins = have && pk < lk1;
+                    if (__any_sync(GHN_FULL, ins)) {
+                        thr_bubble(L, ins ? pk : TT_INF);
+                        lk1 = thr_pick(L, k);
+                    }
+                    wk.step();
+                }
+            }
+            if (more && eq) {   // a shell point shares the k-th key's d-part
+                push_fallback(a, qi);
+                more = false;
+            }
+            if (more) {
+                layers = l;
+                if (STATS) points += thr_shell_count(w, lr, lc, l);
+                bool stop = !lt && a.mode == GHN_MODE_HEURISTIC;
+                if (a.mode == GHN_MODE_GUARANTEED) {
+                    const double b = __dmul_rn((double)l, a.min_w);
+                    const double b2 = __dmul_rn(b, b);
+                    const uint32_t tk = thr_pick(L, k - 1) & ~lmask;
+                    if (b2 >= thr_upper(tk, lmask)) {
+                        stop = true;
+                    } else if (b2 > thr_lower(tk)) {
+                        push_fallback(a, qi);
+                        more = false;
+                    }
+                }
+                if (more && (stop || l >= lmax)) {
+                    more = false;
+                    fin = true;
+                }
+            }
+        }
+        // ---- D: vote and outputs
+        if (fin) {
+            const uint32_t tau = thr_pick(L, k - 1), nx = thr_pick(L, k);
+            int wl, top;
+            if ((nx != TT_INF && (nx & ~lmask) == (tau & ~lmask)) || !thr_vote<KM>(L, k, lmask, wl, top, lmask)) {
+                push_fallback(a, qi);
+            } else {
+                if (a.out_label) a.out_label[qi] = wl;
+                if (a.out_conf) a.out_conf[qi] = __ddiv_rn((double)top, (double)k);
+                if (STATS) {
+                    const int cells = thr_block_cells(w, lr, lc, layers);
+                    if (a.out_stats) {
+                        a.out_stats[3 * (int64_t)qi + 0] = layers;
+                        a.out_stats[3 * (int64_t)qi + 1] = cells;
+                        a.out_stats[3 * (int64_t)qi + 2] = points;
+                    }
+                    tot.layers += layers;
+                    tot.cells += cells;
+                    tot.points += points;
+                    tot.n += 1;
+                }
+            }
+        }
+    }
+}
+
 template <int KM, bool STATS>
 __device__ __forceinline__ void tile2d_thr_body(const T2Args &a) {
     extern __shared__ __align__(16) unsigned char sm[];
@@ -1490,7 +1800,21 @@ __device__ __forceinline__ void tile2d_thr_body(const T2Args &a) {
     __syncthreads();
     const ThrWin w{sxy, sl, loc, R, W, W1};
     ThrTotals tot{0, 0, 0, 0};
-    if constexpr (KM > 0 && KM <= 2) {   // k <= 2: each lane on its own loop
+    if constexpr (KM > 0 && GHN_TT_TAB) {
+        // table-driven rounds (run_rounds_tab): the sort's scratch lives in the row tables
+        __shared__ uint16_t s_ord[SB_SORT_N];
+        __shared__ uint32_t s_info[SB_SORT_N];
+        __shared__ int s_grp;
+        uint32_t *rtab = (uint32_t *)(rstart + a.win + 1);
+        const int nrw = 2 * a.A + 2;
+        for (int c0 = qb; c0 < qe; c0 += SB_SORT_N) {
+            const int c1 = min(c0 + SB_SORT_N, qe);
+            if (threadIdx.x == 0) s_grp = 0;
+            sel_sort_chunk(a, w, c0, c1, t0, t1, r_lo, c_lo, (int *)rtab, (uint16_t *)(rtab + 512), s_ord, s_info, false);
+            run_rounds_tab<KM == 0 ? 1 : KM, STATS>(a, w, rtab, nrw, s_ord, s_info, &s_grp, c0, c1, r_lo, c_lo, tot);
+            __syncthreads();
+        }
+    } else if constexpr (KM > 0 && KM <= 2) {   // k <= 2: each lane on its own loop
         for (int qq = qb + (int)threadIdx.x; qq < qe; qq += TT_THREADS)
             process_query_thr<KM, STATS>(a, w, a.qorder[qq], t0, t1, r_lo, c_lo, tot);
     } else if constexpr (KM == 0) {
@@ -1506,7 +1830,7 @@ __device__ __forceinline__ void tile2d_thr_body(const T2Args &a) {
         for (int c0 = qb; c0 < qe; c0 += SB_SORT_N) {
             const int c1 = min(c0 + SB_SORT_N, qe);
             if (threadIdx.x == 0) s_grp = 0;
-            sel_sort_chunk(a, w, c0, c1, t0, t1, r_lo, c_lo, (int *)hist, (uint16_t *)(hist + 512), s_ord, s_info);
+            sel_sort_chunk(a, w, c0, c1, t0, t1, r_lo, c_lo, (int *)hist, (uint16_t *)(hist + 512), s_ord, s_info, true);
             if (a.lmask > 3)
                 run_rounds_sel<STATS, true>(a, w, hist, rtab, s_ord, s_info, &s_grp, c0, c1, t0, t1, r_lo, c_lo, tot);
             else
@@ -1537,9 +1861,13 @@ __device__ __forceinline__ void tile2d_thr_body(const T2Args &a) {
     }
 }
 
-// k <= 32 (register list): registers as ptxas chooses for 256 threads.
+// k <= 32 (register list): four CTAs per SM up to k = 4, GHN_TT_MINB16 for
+// k = 5-16, two for k = 17-32.
+#ifndef GHN_TT_MINB16
+#define GHN_TT_MINB16 3
+#endif
 template <int KM, bool STATS>
-__global__ void __launch_bounds__(TT_THREADS) tile2d_thr_kernel(const T2Args a) {
+__global__ void __launch_bounds__(TT_THREADS, KM <= 4 ? 4 : (KM <= 16 ? GHN_TT_MINB16 : 2)) tile2d_thr_kernel(const T2Args a) {
     tile2d_thr_body<KM, STATS>(a);
 }
 
