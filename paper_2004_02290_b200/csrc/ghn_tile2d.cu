@@ -1141,10 +1141,21 @@ bool tile2d_plan(const ghn_index_view *ix, int64_t nq, int32_t k, int32_t task, 
     int lf = 0;
     while (lf < 8 && (2.0 * lf + 1) * (2.0 * lf + 1) * rho < (double)k) ++lf;
     // apron: two layers beyond the layer that fills the buffer on average.  The
-    // bucket select without QueryStats needs one: a shell beyond the apron that
+    // thread kernels without QueryStats need one: a shell beyond the apron that
     // provably cannot change the top-k is skipped without its data.
     const bool thr = k <= TT_KMAX && ix->n_labels > 0 && ix->n_labels <= 8;
-    const int extra = thr && k > tt_list_kmax() && !want_stats ? 1 : 2;
+    // (only when block(lf) almost surely fills the buffer: a query that needs
+    // the next block looks two layers out)
+    double p_short = 0.0;   // P(Poisson((2 lf + 1)^2 rho) < k)
+    {
+        const double m = (2.0 * lf + 1) * (2.0 * lf + 1) * rho;
+        double term = exp(-m);
+        for (int i = 0; i < k; ++i) {
+            p_short += term;
+            term *= m / (i + 1);
+        }
+    }
+    const int extra = thr && (k > tt_list_kmax() || tt_tab_on()) && !want_stats && p_short < 1e-3 ? 1 : 2;
     const int A = (int)knob("GHN_TILE_A", lf + extra > 4 ? 4 : lf + extra);
     int T = (int)floor(sqrt(0.7 * T2_CAP / (rho > 1e-9 ? rho : 1e-9))) - 2 * A;
     const double Tmax = sqrt((double)ix->E / (sm_count() * 4.0));

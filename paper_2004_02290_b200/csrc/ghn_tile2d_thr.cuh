@@ -1618,7 +1618,7 @@ __device__ __forceinline__ void run_rounds_tab(const T2Args &a, const ThrWin &w,
         }
         bool more = live && l < lmax;   // continues with layer l + 1
         bool fin = live && !more;       // answered after layer l
-        // ---- C: later layers
+        // ---- C (tab): later layers
         const RectBound rb0 = more ? RectBound(a, q0, q1, cc0, cc1) : RectBound();
         while (__any_sync(GHN_FULL, more)) {
             uint32_t tm = 0;
@@ -1718,7 +1718,7 @@ __device__ __forceinline__ void run_rounds_tab(const T2Args &a, const ThrWin &w,
                 }
             }
         }
-        // ---- D: vote and outputs
+        // ---- D (tab): vote and outputs
         if (fin) {
             const uint32_t tau = thr_pick(L, k - 1), nx = thr_pick(L, k);
             int wl, top;
@@ -1789,6 +1789,11 @@ __device__ __forceinline__ void tile2d_thr_body(const T2Args &a) {
         return;
     }
     for (int e = threadIdx.x; e < R * W1; e += blockDim.x) loc[e] -= delta[e / W1];
+    // (measured and not kept, cfg4 sweep 13.7 ms: coordinates by 4-byte cp.async
+    // into the float2 slots with the labels four loads deep -- 14.1 ms; rows'
+    // ends fetched and scanned by warp 0 beside the offset loads, one barrier
+    // fewer -- 14.3 ms.  Rows start at arbitrary slots, so 16-byte bulk copies
+    // do not apply without a 12-byte-per-point SoA staging that costs a CTA per SM.)
     for (int i = threadIdx.x >> 5; i < R; i += TT_THREADS / 32) {   // warp per row: coalesced copy
         const int p0 = rstart[i], p1 = rstart[i + 1], d = delta[i];
         for (int p = p0 + (int)(threadIdx.x & 31); p < p1; p += 32) {
