@@ -1180,7 +1180,10 @@ bool tile2d_plan(const ghn_index_view *ix, int64_t nq, int32_t k, int32_t task, 
     if (plan->G == 1) {
         // ~TT_Q queries per tile (one or two per thread) within the staging capacity
         const double qd = (double)nq / (double)ix->E;
-        const double tq = knob("GHN_TT_Q", TT_Q);
+        // (the list rounds for k = 5-32 run best with two groups per warp:
+        // cfg4 k = 8 / 16 / 32 at 450 against 256: 2.57 / 2.70 / 6.69 against
+        // 2.92 / 2.91 / 7.10 ms; k <= 4 and the bucket select do not)
+        const double tq = knob("GHN_TT_Q", k > 4 && k <= tt_list_kmax() ? 450.0 : TT_Q);
         int Tq = (int)floor(sqrt(tq / (qd > 1e-9 ? qd : 1e-9)));
         const int Tc = (int)floor(sqrt((TT_CAP - 64.0) / 1.1 / (rho > 1e-9 ? rho : 1e-9))) - 2 * A;
         if (Tq > Tc) Tq = Tc;
