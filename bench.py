@@ -634,7 +634,7 @@ def run_ours(args):
                                f"OpenMP), neighbours only"}
         del ref
         fpp = fp_peaks()
-        for c in [int(x) for x in args.configs.split(",") if x.strip()]:
+        for c in [int(x) for x in args.configs.split(",") if x.strip() and x.strip() != "none"]:
             if c == cfg:
                 continue
             wc = datagen.make(c)

@@ -81,6 +81,7 @@ struct T2Args {
     int32_t sb_capn, sb_redo, sb_wmax, sb_sort, sb_recap;   // bucket-select lock-step knobs (see ghn_tile2d_thr.cuh)
     double tt_skipf;   // k = 3, 4 rounds: skip-ahead threshold (fraction of the block half-width)
     int32_t tt_tab;    // k <= 32: table-driven rounds (run_rounds_tab)
+    double sb_skipf;   // bucket select: skip ahead when the expected k-th radius exceeds this fraction of the block half-width
 };
 
 struct Win {
@@ -1327,6 +1328,7 @@ int32_t tile2d_run(const ghn_index_view *ix, const Tile2dPlan *plan, const void 
     a.sb_sort = (int)knob("GHN_SB_SORT", 1);
     a.tt_skipf = knob("GHN_TT_SKIPF", 0.4);
     a.tt_tab = tt_tab_on();
+    a.sb_skipf = knob("GHN_SB_SKIPF", 0.8);
     const bool stats = out->stats != nullptr || out->totals != nullptr;
     // warp kernel: extraction select for small k (EXT), histogram select otherwise
     int ki = plan->G == 8 ? 1 : (plan->G == 16 ? 2 : (k >= 2 && k <= T2_EXT_MAXK ? 3 : 0));

@@ -437,7 +437,7 @@ __device__ __forceinline__ uint32_t sel_prep(const T2Args &a, const ThrWin &w, i
     uint32_t skip = 0u;
     if (allow_skip && a.mode == GHN_MODE_HEURISTIC && a.q_dtype == GHN_F32 && l < lmax && l + 1 <= a.A && cnt > 0) {
         const double kc = (double)a.k * (2.0 * l + 1.0) * (2.0 * l + 1.0) / (3.14159265358979 * (double)cnt);
-        const double fc = 0.8 * ((double)l + 0.5);
+        const double fc = a.sb_skipf * ((double)l + 0.5);
         if (kc > fc * fc) {
             const int c2 = sel_block_count(w, lr, lc, l + 1);
             if (c2 <= a.sb_capn) {
@@ -893,9 +893,9 @@ __device__ __forceinline__ int sel_bytesum(uint64_t v) {
 // Skip-ahead lanes: is a candidate of block(ls) in shell(ls)?  From fp32
 // coordinates: u = the candidate's Chebyshev distance from the centre of q's
 // cell in units of block(ls-1)'s half-width; u > 1 + eps: surely in the
-// shell, u < 1 - eps: surely inside block(ls-1), else undecided (the query
-// leaves the tile path if such a candidate is a member).  Other lanes carry
-// s = 0: u = 0, always inside.
+// shell, u < 1 - eps: surely inside block(ls-1), else the point's own cell
+// decides (exact re-keying pass).  Other lanes carry s = 0: u = 0, always
+// inside.
 struct SelGeo {
     float s0, s1, o0, o1;
     __device__ __forceinline__ float u(float dx, float dy) const {
@@ -905,9 +905,9 @@ struct SelGeo {
 constexpr float SEL_GEO_LO = 1.0f - 3e-6f, SEL_GEO_HI = 1.0f + 3e-6f;   // fp32 rounding of u: < 1e-6
 
 // Pass 2 for the whole warp.  Sure members are voted into cn; the slots of
-// the candidates to re-key are noted at note[j * TT_THREADS] (low half).
-// SKIP: geo counts the sure members beyond SEL_GEO_LO (low half) and beyond
-// SEL_GEO_HI (high half).
+// the candidates to re-key are noted at note[j * TT_THREADS] (low half);
+// `noted` may exceed SB_NOTE (SKIP only): the caller gives up then.
+// SKIP: geo != 0 iff a sure member lies in shell(ls).
 template <bool SKIP, bool WIDE>
 __device__ __forceinline__ void sel_pass2(uint32_t xy_s, uint32_t sl_s, uint32_t myr_s, uint32_t note_s, bool sel, int n,
                                           int steps, float q0f, float q1f, uint32_t tlo, uint32_t span,
@@ -916,6 +916,7 @@ __device__ __forceinline__ void sel_pass2(uint32_t xy_s, uint32_t sl_s, uint32_t
     typedef typename SelCnt<WIDE>::type cnt_t;
     cnt_t cn = 0;
     uint32_t geo = 0u;
+    int nnote = 0;
     uint32_t np = note_s;
     SelWalk wk;
     wk.start(myr_s, sel);
@@ -928,24 +929,34 @@ __device__ __forceinline__ void sel_pass2(uint32_t xy_s, uint32_t sl_s, uint32_t
         const bool have = it < n2;
         const bool low = have && bits < tlo;
         const bool amb = have && (uint32_t)(bits - tlo) < span;
+        bool vote = low, note = amb;
+        if (SKIP) {
+            // a sure member whose cell the fp32 coordinates cannot place (on a
+            // cell boundary of block(ls-1), common for fp32 data on a power-of-two
+            // grid) is noted too: the re-keying places it exactly
+            const float u = g.u(dx, dy);
+            const bool band = low && u > SEL_GEO_LO && !(u > SEL_GEO_HI);
+            geo |= low && u > SEL_GEO_HI ? 1u : 0u;
+            vote = low && !band;
+            note = amb || band;
+            nnote += note ? 1 : 0;
+        }
         if (WIDE) {
             const uint64_t inc = 1ull << lab8;
-            cn += low ? (cnt_t)inc : (cnt_t)0;
+            cn += vote ? (cnt_t)inc : (cnt_t)0;
         } else {
             const uint32_t inc = __funnelshift_l(0u, 1u, lab8);   // 1 << lab8, lab8 <= 24
-            cn += low ? (cnt_t)inc : (cnt_t)0;
+            cn += vote ? (cnt_t)inc : (cnt_t)0;
         }
-        if (SKIP) {
-            const float u = g.u(dx, dy);
-            geo += low && u > SEL_GEO_LO ? 1u : 0u;
-            geo += low && u > SEL_GEO_HI ? 0x10000u : 0u;
-        }
-        if (amb) asm volatile("st.shared.u16 [%0], %1;" ::"r"(np), "h"((uint16_t)wk.p) : "memory");
-        np += amb ? TT_THREADS * 4 : 0;
+        if (note) asm volatile("st.shared.u16 [%0], %1;" ::"r"(np), "h"((uint16_t)wk.p) : "memory");
+        np += note ? TT_THREADS * 4 : 0;
+        // (SKIP: the histogram does not bound the boundary members; past the
+        // lane's SB_NOTE words the last one is overwritten and the count tells)
+        if (SKIP) np = min(np, note_s + (uint32_t)(SB_NOTE - 1) * TT_THREADS * 4);
         wk.step();
     }
     cn_out = cn;
-    noted = (int)((np - note_s) / (TT_THREADS * 4));
+    noted = SKIP ? nnote : (int)((np - note_s) / (TT_THREADS * 4));
     geo_out = geo;
 }
 
@@ -1189,7 +1200,11 @@ __device__ __forceinline__ void run_rounds_sel(const T2Args &a, const ThrWin &w,
             for (int j = 0; j <= SB_C; ++j) Lb[j] = TT_INF;
             cnt_t cnx = 0;
             int nlx = 0, nlist = 0;
-            bool chg = (geoc >> 16) != 0u, geo_bad = (geoc >> 16) != (geoc & 0xffffu);
+            bool chg = geoc != 0u;
+            if (sel && noted > SB_NOTE) {   // more boundary members than a lane can note
+                { FB_REASON(9); push_fallback(a, qi); }
+                sel = false;
+            }
             {
                 const int nn = sel ? noted : 0;
                 const int nmax = __reduce_max_sync(GHN_FULL, nn);
@@ -1202,7 +1217,13 @@ __device__ __forceinline__ void run_rounds_sel(const T2Args &a, const ThrWin &w,
                     if (anyskip) {
                         const float u = geo.u(__fsub_rn(c.x, q0f), __fsub_rn(c.y, q1f));
                         insh = u > SEL_GEO_HI;
-                        ingeo = u > SEL_GEO_LO && !insh;
+                        ingeo = on && skipm && u > SEL_GEO_LO && !insh;
+                        if (__any_sync(GHN_FULL, ingeo)) {   // on a boundary of block(ls-1): the point's own cell decides
+                            const int64_t e0 = cell_id((double)c.x, a.w0, a.inv0, a.pow2 & 1u) - a.lo0 - cc0;
+                            const int64_t e1 = cell_id((double)c.y, a.w1, a.inv1, (a.pow2 >> 1) & 1u) - a.lo1 - cc1;
+                            const int64_t ch = max(e0 < 0 ? -e0 : e0, e1 < 0 ? -e1 : e1);
+                            insh = ingeo ? ch >= (int64_t)ls : insh;
+                        }
                     }
                     const uint32_t pk = thr_pack(c, q0, q1, (lab8 >> 3) | (insh ? lmask + 1u : 0u), fmask);
                     const bool lowx = on && pk < plo;
@@ -1211,7 +1232,6 @@ __device__ __forceinline__ void run_rounds_sel(const T2Args &a, const ThrWin &w,
                     nlx += lowx ? 1 : 0;
                     nlist += lst ? 1 : 0;
                     chg |= lowx && insh;
-                    geo_bad |= on && ingeo;   // (conservative: also when the candidate ends up beyond the k-th)
                     thr_bubble(Lb, lst ? pk : TT_INF);
                 }
             }
@@ -1258,7 +1278,6 @@ __device__ __forceinline__ void run_rounds_sel(const T2Args &a, const ThrWin &w,
                 cls = cnt;
                 // layer ls filled / changed the buffer, or (skip mode) changed iff a shell member
                 const bool changed = !skipm || chg;
-                bad |= skipm && geo_bad;
                 skipm = false;
                 stop = !changed;
                 // the next listed candidate shares the k-th's d-part: undecidable
