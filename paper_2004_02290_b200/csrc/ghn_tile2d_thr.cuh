@@ -43,6 +43,16 @@
 namespace ghn {
 namespace {
 
+// Bounds checks of the shared-memory walks, tables and note buffers: device
+// asserts in a -DGHN_ASSERTS build (compute-sanitizer is closed on this GPU
+// pool; tools/asserts.sh runs the GPU parity tests on such a build).
+#ifdef GHN_ASSERTS
+#include <assert.h>
+#define GHN_ASSERT(c) assert(c)
+#else
+#define GHN_ASSERT(c) ((void)0)
+#endif
+
 constexpr int TT_THREADS = 256;
 #ifndef GHN_TT_TAB
 #define GHN_TT_TAB 1   // k <= 32: table-driven rounds (run_rounds_tab); 0: the round-1 rounds, for A/B builds
@@ -948,6 +958,7 @@ __device__ __forceinline__ void sel_pass2(uint32_t xy_s, uint32_t sl_s, uint32_t
             const uint32_t inc = __funnelshift_l(0u, 1u, lab8);   // 1 << lab8, lab8 <= 24
             cn += vote ? (cnt_t)inc : (cnt_t)0;
         }
+        GHN_ASSERT(wk.p >= 0 && wk.p < 65536 && np < note_s + (uint32_t)SB_NOTE * TT_THREADS * 4);
         if (note) asm volatile("st.shared.u16 [%0], %1;" ::"r"(np), "h"((uint16_t)wk.p) : "memory");
         np += note ? TT_THREADS * 4 : 0;
         // (SKIP: the histogram does not bound the boundary members; past the
@@ -1088,6 +1099,7 @@ __device__ __forceinline__ void run_rounds_sel(const T2Args &a, const ThrWin &w,
                     int s = 0, e = 0;
                     if (rowon) thr_rect_slots(w, lr, lc, ra, ca, cb, s, e);
                     if (e > s) {
+                        GHN_ASSERT(jw < SB_ROWS - 1 && e <= a.cap);
                         myr[jw * TT_THREADS] = (uint32_t)s | ((uint32_t)e << 16);
                         ++jw;
                         n += e - s;
@@ -1105,6 +1117,7 @@ __device__ __forceinline__ void run_rounds_sel(const T2Args &a, const ThrWin &w,
                 wk.start(myr_s, need);
                 const int kb = SB_F32_SHIFT - bbase;
                 for (int it = 0; it < steps; ++it) {
+                    GHN_ASSERT(wk.p >= 0 && wk.p <= a.cap);
                     const float2 c = lds_f2(xy_s + 8u * (uint32_t)wk.p);
                     const uint32_t bits = sb_bits32(__fsub_rn(c.x, q0f), __fsub_rn(c.y, q1f));
                     const int b = sb_clamp((int)(bits >> SB_F32_S) + kb, SB_NB - 1);
@@ -1210,7 +1223,9 @@ __device__ __forceinline__ void run_rounds_sel(const T2Args &a, const ThrWin &w,
                 const int nmax = __reduce_max_sync(GHN_FULL, nn);
                 for (int j = 0; j < nmax; ++j) {
                     const bool on = j < nn;
+                    GHN_ASSERT(j < SB_NOTE);
                     const int slot = on ? (int)(myh[j * TT_THREADS] & 0xffffu) : 0;
+                    GHN_ASSERT(slot >= 0 && slot < a.cap);
                     const float2 c = w.xy[slot];
                     const uint32_t lab8 = (uint32_t)w.sl[slot];
                     bool insh = false, ingeo = false;
@@ -1584,6 +1599,7 @@ __device__ __forceinline__ void run_rounds_tab(const T2Args &a, const ThrWin &w,
                     int s = 0, e = 0;
                     if (rowon) thr_rect_slots(w, lr, lc, ra, ca, cb, s, e);
                     if (e > s) {
+                        GHN_ASSERT(jw < nrw - 1 && e <= a.cap);
                         myr[jw * TT_THREADS] = (uint32_t)s | ((uint32_t)e << 16);
                         ++jw;
                         n += e - s;
@@ -1600,6 +1616,7 @@ __device__ __forceinline__ void run_rounds_tab(const T2Args &a, const ThrWin &w,
                 uint32_t bt[8];
 #pragma unroll
                 for (int u = 0; u < 8; ++u) {
+                    GHN_ASSERT(wk.p >= 0 && wk.p <= a.cap);
                     const uint32_t pk = tab_pack(xy_s, sl_s, wk.p, q0, q1, lmask);
                     bt[u] = it + u < n ? pk : TT_INF;
                     wk.step();
@@ -1701,6 +1718,7 @@ __device__ __forceinline__ void run_rounds_tab(const T2Args &a, const ThrWin &w,
                 uint32_t lk1 = thr_pick(L, k);   // a candidate at or beyond the (k+1)-th leaves L[0..k] alone
                 for (int it = 0; it < steps; ++it) {
                     const bool have = it < n;
+                    GHN_ASSERT(wk.p >= 0 && wk.p <= a.cap);
                     const uint32_t pk = tab_pack(xy_s, sl_s, wk.p, q0, q1, lmask);
                     lt |= have && pk < tm;
                     eq |= have && (uint32_t)(pk - tm) <= lmask;
