@@ -23,3 +23,6 @@ timeout 120 python tools/fit_launches.py > $O/fl_plain.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
     --log-file $O/fit_launches.csv python tools/fit_launches.py > $O/fl_ncu.log 2>&1
 echo "fit launch list rc=$?"
+# issue-slot captures of the timed kernels (k = 64 bucket select, k = 16 list rounds): --set full, source on
+KREGEX=tile2d_sel bash tools/prof_cmd.sh sel64 64 10000000 | tail -1
+KREGEX=tile2d_thr_kernel bash tools/prof_cmd.sh thr16 16 10000000 | tail -1
