@@ -85,13 +85,13 @@ def peaks():
 
 def issue_roofline():
     """Issue-slot roofline of the predict kernel from the committed ncu capture."""
-    p = os.path.join(REPO, "profiles", "ncu_issue_r01.json")
+    p = os.path.join(REPO, "profiles", "ncu_issue_r02.json")
     try:
         with open(p) as fh:
             m = json.load(fh)
         return {k: {"issue_active_frac": v["issue_active_frac"],
                     "warp_instructions_per_query": v["warp_instructions_per_query"]}
-                for k, v in m.items() if k.startswith("k")} | {"source": "profiles/ncu_issue_r01.json"}
+                for k, v in m.items() if k.startswith("k")} | {"source": "profiles/ncu_issue_r02.json"}
     except Exception:
         return None
 
@@ -596,7 +596,7 @@ def run_ours(args):
                            "the first H2D and the last D2H are exposed; no L2 flush (training data 800 MB > L2)"}
 
     # ---- CPU legs, parity of the timed outputs, other configs (rank 0, N=1 only)
-    cpu_baseline = cpu_c = fit_cpu = parity = None
+    cpu_baseline = cpu_c = fit_cpu = parity = neighbors = None
     configs = {}
     if rank == 0 and world == 1:
         import oracle
@@ -632,6 +632,37 @@ def run_ours(args):
             cpu_c = {"value": len(ks) * mq / (time.perf_counter() - t0), "unit": "queries/s", "cores": th,
                      "sample": f"{mq} queries x k in {ks}, oracle/ghn_oracle.c (dense ring enumeration, "
                                f"OpenMP), neighbours only"}
+        # ---- neighbour-returning predict (knn_query_batch, explore.py:132-137) at k = 16
+        if cfg == 4 and 16 in ks:
+            from paper_2004_02290_b200 import knn_query_batch
+
+            kn = 16
+            for _ in range(2):
+                knn_query_batch(index, Q_d, kn, stats=False)
+            torch.cuda.synchronize()
+            tms = []
+            for _ in range(3):
+                flush.zero_()
+                torch.cuda.synchronize()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                dist_n, idx_n, _ = knn_query_batch(index, Q_d, kn, stats=False)
+                e1.record(stream)
+                torch.cuda.synchronize()
+                tms.append(e0.elapsed_time(e1))
+            rng = np.random.default_rng(7100)
+            sel = np.sort(rng.choice(nq, size=min(args.parity_sample, nq), replace=False))
+            keys_r, idx_r, _ = ref.query(w.Q[sel], kn, "heuristic")
+            sel_d = torch.from_numpy(sel).to(dev)
+            bad = int(np.count_nonzero((idx_n[sel_d].cpu().numpy() != idx_r).any(axis=1) |
+                                       (dist_n[sel_d].cpu().numpy() != np.sqrt(keys_r)).any(axis=1)))
+            neighbors = {"k": kn, "queries_per_s": nq / (statistics.median(tms) / 1e3), "ms": statistics.median(tms),
+                         "output_bytes": int(nq * kn * 16),
+                         "what": "knn_query_batch: (nq, k) fp64 distances + int64 point indices, no QueryStats",
+                         "parity_checked": {"ok": bad == 0, "queries": int(sel.size), "mismatches": bad,
+                                            "checked": "indices + distances (bit-exact)",
+                                            "against": "oracle/ghn_oracle.c"}}
+            del dist_n, idx_n
         del ref
         fpp = fp_peaks()
         for c in [int(x) for x in args.configs.split(",") if x.strip() and x.strip() != "none"]:
@@ -675,6 +706,7 @@ def run_ours(args):
                          "issue_roofline": issue_roofline(),
                          "kernel_stats": ncu_kernel_stats(cfg, ks)},
             "parity_checked": parity,
+            "neighbors": neighbors,
             "e2e": e2e,
             "gpu_launches": m["launches"] // args.steps,
             "gpu_launches_total": m["launches"],

@@ -71,6 +71,8 @@ struct T2Args {
     int32_t T, A, nt0, nt1, win, cap;
     int32_t *out_label;
     double *out_conf;
+    double *out_dist;    // neighbours (tile2d_nb_kernel): (nq, k) exact keys, then distances
+    int64_t *out_idx;    //                                (nq, k) point indices
     int64_t *out_stats;
     unsigned long long *totals;
     int32_t *fb_list;
@@ -1124,6 +1126,10 @@ static int tt_tab_on() {
     return GHN_TT_TAB;
 }
 
+static int tt_list_kmax_nb() {
+    return TT_LIST_KMAX;
+}
+
 static int tt_list_kmax() {
     return (int)knob("GHN_TT_LISTMAX", TT_LIST_KMAX);
 }
@@ -1132,7 +1138,9 @@ bool tile2d_plan(const ghn_index_view *ix, int64_t nq, int32_t k, int32_t task, 
                  Tile2dPlan *plan) {
     memset(plan, 0, sizeof(*plan));
     if (ix->layout != GHN_LAYOUT_DENSE || ix->d != 2 || ix->dtype != GHN_F32) return false;
-    if (task != GHN_TASK_CLASSIFY || want_neighbors || !ix->labels_perm) return false;
+    // the fused vote, or (list rounds, k <= 32) the neighbours alone
+    const bool nb = task == GHN_TASK_NONE && want_neighbors && GHN_TT_TAB != 0 && k <= tt_list_kmax_nb();
+    if (!nb && (task != GHN_TASK_CLASSIFY || want_neighbors || !ix->labels_perm)) return false;
     if (ix->metric != GHN_METRIC_EUCLIDEAN) return false;
     if (nq < 4096 || k < 1 || k > 256) return false;
     // points per cell to size tiles for: the mean, or the caller's local
@@ -1144,7 +1152,7 @@ bool tile2d_plan(const ghn_index_view *ix, int64_t nq, int32_t k, int32_t task, 
     // apron: two layers beyond the layer that fills the buffer on average.  The
     // thread kernels without QueryStats need one: a shell beyond the apron that
     // provably cannot change the top-k is skipped without its data.
-    const bool thr = k <= TT_KMAX && ix->n_labels > 0 && ix->n_labels <= 8;
+    const bool thr = nb || (k <= TT_KMAX && ix->n_labels > 0 && ix->n_labels <= 8);
     // (only when block(lf) almost surely fills the buffer: a query that needs
     // the next block looks two layers out)
     double p_short = 0.0;   // P(Poisson((2 lf + 1)^2 rho) < k)
@@ -1178,6 +1186,8 @@ bool tile2d_plan(const ghn_index_view *ix, int64_t nq, int32_t k, int32_t task, 
     // thread per query (packed-key register list): k <= 32, <= 8 label codes
     if (k <= TT_KMAX && ix->n_labels > 0 && ix->n_labels <= 8) plan->G = 1;
     plan->G = (int)knob("GHN_TILE_G", plan->G);
+    if (nb) plan->G = 1;
+    plan->nb = nb ? 1 : 0;
     if (plan->G == 1) {
         // ~TT_Q queries per tile (one or two per thread) within the staging capacity
         const double qd = (double)nq / (double)ix->E;
@@ -1312,6 +1322,8 @@ int32_t tile2d_run(const ghn_index_view *ix, const Tile2dPlan *plan, const void 
     a.cap = plan->cap;
     a.out_label = out->label;
     a.out_conf = out->confidence;
+    a.out_dist = out->dist;
+    a.out_idx = out->idx;
     a.out_stats = out->stats;
     a.totals = out->totals;
     a.fb_list = fbl;
@@ -1350,11 +1362,22 @@ int32_t tile2d_run(const ghn_index_view *ix, const Tile2dPlan *plan, const void 
             (const void *)tile2d_thr_kernel<16, false>, (const void *)tile2d_thr_kernel<16, true>,
             (const void *)tile2d_thr_kernel<32, false>, (const void *)tile2d_thr_kernel<32, true>};
         fn = thr_fns[ki - 4];
+        if (plan->nb) {
+            static const void *const nb_fns[12] = {
+                (const void *)tile2d_nb_kernel<1, false>,  (const void *)tile2d_nb_kernel<1, true>,
+                (const void *)tile2d_nb_kernel<2, false>,  (const void *)tile2d_nb_kernel<2, true>,
+                (const void *)tile2d_nb_kernel<4, false>,  (const void *)tile2d_nb_kernel<4, true>,
+                (const void *)tile2d_nb_kernel<8, false>,  (const void *)tile2d_nb_kernel<8, true>,
+                (const void *)tile2d_nb_kernel<16, false>, (const void *)tile2d_nb_kernel<16, true>,
+                (const void *)tile2d_nb_kernel<32, false>, (const void *)tile2d_nb_kernel<32, true>};
+            fn = nb_fns[ki - 6];
+            ki += 14;   // (its own slot in the shared-memory attribute table)
+        }
     }
     // largest dynamic smem opted into, per device and kernel (function
     // attributes are per device; callers may run on several devices / threads)
     static std::mutex attr_mu;
-    static size_t attr_smem[64][20] = {};
+    static size_t attr_smem[64][36] = {};
     int dev = 0;
     GHN_CUDA_CHECK(cudaGetDevice(&dev));
     std::lock_guard<std::mutex> attr_lock(attr_mu);
@@ -1377,6 +1400,13 @@ int32_t tile2d_run(const ghn_index_view *ix, const Tile2dPlan *plan, const void 
     else
         tile2d_kernel<false><<<nb, T2_THREADS, plan->smem, s>>>(a);
     GHN_LAUNCH_CHECK("tile2d_kernel");
+    if (plan->nb) {   // order every row by (key, index), keys -> distances (fallback rows are rewritten later)
+        int P = 1;
+        while (P < k) P <<= 1;
+        const int64_t warps = (nq + 32 / P - 1) / (32 / P);
+        nb_sort_kernel<<<(unsigned)((warps + 7) / 8), 256, 0, s>>>(out->dist, out->idx, nq, k, P, ix->perm, ix->n);
+        GHN_LAUNCH_CHECK("nb_sort_kernel");
+    }
     if (knob("GHN_DEBUG_FALLBACK", 0) != 0) {   // diagnostics: queries sent to the generic kernel
         int32_t nfb = 0;
         cudaMemcpyAsync(&nfb, fbc, 4, cudaMemcpyDeviceToHost, s);

@@ -11,13 +11,15 @@ struct Tile2dPlan {
     int32_t nt0, nt1; // tiles per dimension
     int64_t ntiles;
     int32_t win;      // T + 2A
-    int32_t G;        // lanes per query (32: warp kernel; 8/16: group kernel)
+    int32_t G;        // lanes per query (32: warp kernel; 8/16: group kernel; 1: thread kernels)
+    int32_t nb;       // neighbours instead of the vote (thread kernel, list rounds)
     int32_t cap;      // staged points per CTA
     size_t smem;      // dynamic shared memory per CTA
 };
 
-// Whether the tiled path applies (2-D, DENSE, fp32, classify without
-// neighbour output) and its geometry for this k.
+// Whether the tiled path applies (2-D, DENSE, fp32; the fused vote without
+// neighbour output, or -- k <= 32 -- the neighbours alone) and its geometry
+// for this k.
 // want_stats: QueryStats / totals are requested (the bucket select then stages one more apron layer).
 bool tile2d_plan(const ghn_index_view *ix, int64_t nq, int32_t k, int32_t task, bool want_neighbors, bool want_stats,
                  Tile2dPlan *plan);

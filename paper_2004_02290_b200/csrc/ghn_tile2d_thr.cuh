@@ -64,6 +64,8 @@ struct ThrWin {
     const uint8_t *sl;     // staged label codes
     const int32_t *loc;    // (R, W+1) local slot of each cell start
     int R, W, W1;
+    const int32_t *rstart; // (R+1) first staged slot of each window row
+    const int32_t *delta;  // (R) global CSR slot = staged slot + delta[row]
 };
 
 // Range r of shell(l) (l = 0: the centre cell; l >= 1: 4l ranges -- the full
@@ -118,6 +120,13 @@ __device__ __forceinline__ uint32_t thr_pack(float2 c, double q0, double q1, uin
     const double key = __dadd_rn(__dmul_rn(d0, d0), __dmul_rn(d1, d1));
     const uint32_t top = __funnelshift_l((uint32_t)__double2loint(key), (uint32_t)__double2hiint(key), 1);
     return (top & ~lmask) | lab;
+}
+
+// The exact key itself (the same operations as thr_pack).
+__device__ __forceinline__ double thr_key(float2 c, double q0, double q1) {
+    const double d0 = __dsub_rn((double)c.x, q0);
+    const double d1 = __dsub_rn((double)c.y, q1);
+    return __dadd_rn(__dmul_rn(d0, d0), __dmul_rn(d1, d1));
 }
 
 // Keys whose d-part is D (label bits cleared) lie in [lower, upper).
@@ -1519,12 +1528,12 @@ __device__ __forceinline__ uint32_t tab_pack(uint32_t xy_s, uint32_t sl_s, int p
     return thr_pack(lds_f2(xy_s + 8u * (uint32_t)p), q0, q1, lds_u8(sl_s + (uint32_t)p), lmask);
 }
 
-template <int KM, bool STATS>
+template <int KM, bool STATS, bool NB>
 __device__ __forceinline__ void run_rounds_tab(const T2Args &a, const ThrWin &w, uint32_t *rtab, int nrw,
                                                const uint16_t *ord, const uint32_t *info, int *s_grp, int qb, int qe,
                                                int r_lo, int c_lo, ThrTotals &tot) {
     const int k = a.k;
-    const uint32_t lmask = (uint32_t)a.lmask;
+    const uint32_t lmask = NB ? 0u : (uint32_t)a.lmask;   // (neighbours: no label bits, the staged codes are zero)
     uint32_t *myr = rtab + threadIdx.x;   // row-table word j at myr[j * TT_THREADS]
     const uint32_t myr_s = sm_addr(myr), xy_s = sm_addr(w.xy), sl_s = sm_addr(w.sl);
     for (;;) {
@@ -1755,6 +1764,84 @@ __device__ __forceinline__ void run_rounds_tab(const T2Args &a, const ThrWin &w,
                 }
             }
         }
+        // ---- D (tab), neighbours (explore.py:132-137): the members are the
+        // candidates of block(layers) whose d-part does not exceed the k-th's
+        // (exactly k when the (k+1)-th has another d-part).  They are walked
+        // once more -- rows clipped to the k-th radius -- and written with their
+        // exact keys and CSR slots, unordered; nb_sort_kernel maps the slots to
+        // point indices, orders each row by (key, index) and takes the square roots.
+        if constexpr (NB) {
+            const uint32_t tau = fin ? thr_pick(L, k - 1) : 0u, nx = fin ? thr_pick(L, k) : TT_INF;
+            if (fin && nx != TT_INF && (nx & ~lmask) == (tau & ~lmask)) {
+                push_fallback(a, qi);
+                fin = false;
+            }
+            const uint32_t tm = tau & ~lmask;
+            int n = 0;
+            {
+                const int nrows = fin ? 2 * layers + 1 : 0;
+                const int rmax = __reduce_max_sync(GHN_FULL, nrows);
+                const float r2f = (float)thr_upper(tm, lmask) * 1.0001f;
+                int jw = 0;
+                for (int j = 0; j < rmax; ++j) {
+                    const int ra = j - layers;
+                    int ca = -layers, cb = layers;
+                    const bool rowon = clip.cols(ra, layers, r2f, ca, cb) && j < nrows;
+                    int s0 = 0, e0 = 0;
+                    if (rowon) thr_rect_slots(w, lr, lc, ra, ca, cb, s0, e0);
+                    if (e0 > s0) {
+                        GHN_ASSERT(jw < nrw - 1);
+                        myr[jw * TT_THREADS] = (uint32_t)s0 | ((uint32_t)e0 << 16);
+                        ++jw;
+                        n += e0 - s0;
+                    }
+                }
+                myr[jw * TT_THREADS] = SB_SENT;
+            }
+            const int steps = __reduce_max_sync(GHN_FULL, n);
+            SelWalk wk;
+            wk.start(myr_s, fin);
+            int m = 0;   // members written
+            for (int it = 0; it < steps; ++it) {
+                const int p = wk.p;
+                const float2 c = lds_f2(xy_s + 8u * (uint32_t)p);
+                const uint32_t pk = thr_pack(c, q0, q1, 0u, lmask);
+                const bool mem = it < n && pk <= tm;
+                if (__any_sync(GHN_FULL, mem)) {
+                    if (mem && m < k) {
+                        int lo = 0, hi = w.R - 1;   // the window row holding slot p
+                        while (lo < hi) {
+                            const int mid = (lo + hi + 1) >> 1;
+                            if (w.rstart[mid] <= p) lo = mid;
+                            else hi = mid - 1;
+                        }
+                        // (the CSR slot; nb_sort_kernel turns it into the point index: a
+                        // dependent global load here would stall the lock-step walk)
+                        a.out_dist[(int64_t)qi * k + m] = thr_key(c, q0, q1);
+                        a.out_idx[(int64_t)qi * k + m] = (int64_t)(p + w.delta[lo]);
+                    }
+                    m += mem ? 1 : 0;
+                }
+                wk.step();
+            }
+            if (fin && m != k) {   // (cannot happen with a clean k-th boundary; the generic kernel decides)
+                push_fallback(a, qi);
+                fin = false;
+            }
+            if (fin && STATS) {
+                const int cells = thr_block_cells(w, lr, lc, layers);
+                if (a.out_stats) {
+                    a.out_stats[3 * (int64_t)qi + 0] = layers;
+                    a.out_stats[3 * (int64_t)qi + 1] = cells;
+                    a.out_stats[3 * (int64_t)qi + 2] = points;
+                }
+                tot.layers += layers;
+                tot.cells += cells;
+                tot.points += points;
+                tot.n += 1;
+            }
+            fin = false;   // (nothing left for the vote below)
+        }
         // ---- D (tab): vote and outputs
         if (fin) {
             const uint32_t tau = thr_pick(L, k - 1), nx = thr_pick(L, k);
@@ -1781,7 +1868,7 @@ __device__ __forceinline__ void run_rounds_tab(const T2Args &a, const ThrWin &w,
     }
 }
 
-template <int KM, bool STATS>
+template <int KM, bool STATS, bool NB = false>
 __device__ __forceinline__ void tile2d_thr_body(const T2Args &a) {
     extern __shared__ __align__(16) unsigned char sm[];
     __shared__ int s_P;
@@ -1836,11 +1923,11 @@ __device__ __forceinline__ void tile2d_thr_body(const T2Args &a) {
         for (int p = p0 + (int)(threadIdx.x & 31); p < p1; p += 32) {
             sxy[p] = make_float2(__ldg(a.c0 + p + d), __ldg(a.c1 + p + d));
             // the bucket select keeps label code * 8: its vote is one shift and one add
-            sl[p] = (uint8_t)(KM == 0 ? __ldg(a.labels_perm + p + d) << 3 : __ldg(a.labels_perm + p + d));
+            sl[p] = NB ? (uint8_t)0 : (uint8_t)(KM == 0 ? __ldg(a.labels_perm + p + d) << 3 : __ldg(a.labels_perm + p + d));
         }
     }
     __syncthreads();
-    const ThrWin w{sxy, sl, loc, R, W, W1};
+    const ThrWin w{sxy, sl, loc, R, W, W1, rstart, delta};
     ThrTotals tot{0, 0, 0, 0};
     if constexpr (KM > 0 && GHN_TT_TAB) {
         // table-driven rounds (run_rounds_tab): the sort's scratch lives in the row tables
@@ -1853,7 +1940,7 @@ __device__ __forceinline__ void tile2d_thr_body(const T2Args &a) {
             const int c1 = min(c0 + SB_SORT_N, qe);
             if (threadIdx.x == 0) s_grp = 0;
             sel_sort_chunk(a, w, c0, c1, t0, t1, r_lo, c_lo, (int *)rtab, (uint16_t *)(rtab + 512), s_ord, s_info, false);
-            run_rounds_tab<KM == 0 ? 1 : KM, STATS>(a, w, rtab, nrw, s_ord, s_info, &s_grp, c0, c1, r_lo, c_lo, tot);
+            run_rounds_tab<KM == 0 ? 1 : KM, STATS, NB>(a, w, rtab, nrw, s_ord, s_info, &s_grp, c0, c1, r_lo, c_lo, tot);
             __syncthreads();
         }
     } else if constexpr (KM > 0 && KM <= 2) {   // k <= 2: each lane on its own loop
@@ -1911,6 +1998,44 @@ __device__ __forceinline__ void tile2d_thr_body(const T2Args &a) {
 template <int KM, bool STATS>
 __global__ void __launch_bounds__(TT_THREADS, KM <= 4 ? 4 : (KM <= 16 ? GHN_TT_MINB16 : 2)) tile2d_thr_kernel(const T2Args a) {
     tile2d_thr_body<KM, STATS>(a);
+}
+
+// The same rounds returning the neighbours (knn_query_batch): unordered rows
+// of (exact key, CSR slot), finished by nb_sort_kernel.
+template <int KM, bool STATS>
+__global__ void __launch_bounds__(TT_THREADS, KM <= 4 ? 4 : (KM <= 16 ? GHN_TT_MINB16 : 2)) tile2d_nb_kernel(const T2Args a) {
+    tile2d_thr_body<KM, STATS, true>(a);
+}
+
+// One row of k (key, CSR slot) pairs per group of P = 2^ceil(log2 k) lanes:
+// point index = perm[slot], then a bitonic sort by (key, index) -- the reference's lexsort order,
+// explore.py:114 -- then distance = sqrt(key) (core.py:88-91).
+__global__ void __launch_bounds__(256) nb_sort_kernel(double *__restrict__ dist, int64_t *__restrict__ idx, int64_t nq, int k,
+                                                      int P, const int32_t *__restrict__ perm, int64_t n) {
+    const int lane = (int)(threadIdx.x & 31), sub = lane & (P - 1);
+    const int64_t per_warp = 32 / P;
+    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t q = warp * per_warp + lane / P;
+    const bool on = q < nq && sub < k;
+    double key = on ? dist[q * k + sub] : __longlong_as_double(0x7ff0000000000000LL);
+    long long id = on ? idx[q * k + sub] : 0x7fffffffffffffffLL;
+    // CSR slot -> point index (rows the tile kernel left to the generic kernel hold anything)
+    if (on && id >= 0 && id < n) id = (long long)__ldg(perm + id);
+    for (int size = 2; size <= P; size <<= 1)
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            const double ok = __shfl_xor_sync(GHN_FULL, key, stride);
+            const long long oi = __shfl_xor_sync(GHN_FULL, id, stride);
+            const bool up = (sub & size) == 0;            // ascending half
+            const bool lower = (sub & stride) == 0;       // keeps the smaller of the pair when ascending
+            const bool mine_first = key < ok || (key == ok && id < oi);
+            const bool keep = (lower == up) ? mine_first : !mine_first;
+            key = keep ? key : ok;
+            id = keep ? id : oi;
+        }
+    if (on) {
+        dist[q * k + sub] = __dsqrt_rn(key);
+        idx[q * k + sub] = id;
+    }
 }
 
 // k > 32 (bucket select): three CTAs per SM (<= 80 registers).

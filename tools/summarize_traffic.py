@@ -26,9 +26,16 @@ def summarize(paths_by_k, src):
         # the timed step = the last launch of the main kernel and anything after it in the same predict
         items = list(launches.items())
         names = [n for (_, n), _ in items]
-        main = [i for i, n in enumerate(names) if "tile2d" in n] or list(range(len(names)))
+        # (the vote kernels; the bench's neighbour block runs tile2d_nb_kernel afterwards)
+        main = [i for i, n in enumerate(names) if "tile2d_thr_kernel" in n or "tile2d_sel_kernel" in n] or \
+               [i for i, n in enumerate(names) if "tile2d" in n] or list(range(len(names)))
         last = main[-1]
-        step = [items[last]] + [it for it in items[last + 1:] if "query_kernel" in it[0][1]]
+        step = [items[last]]
+        for it in items[last + 1:]:
+            if "tile2d" in it[0][1]:
+                break
+            if "query_kernel" in it[0][1]:
+                step.append(it)
         b = sum(m.get("dram__bytes_read.sum", 0) + m.get("dram__bytes_write.sum", 0) for _, m in step)
         t = sum(m.get("gpu__time_duration.sum", 0) for _, m in step)
         m0 = step[0][1]
@@ -43,7 +50,7 @@ def summarize(paths_by_k, src):
 if __name__ == "__main__":
     d = sys.argv[1] if len(sys.argv) > 1 else "gpurun_out"
     s = summarize({k: f"{d}/traffic_k{k}.csv" for k in ("1", "4", "16", "64")},
-                  "profiles/traffic_r01_k*.csv (ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,"
+                  "profiles/traffic_r02_k*.csv (ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,"
                   "dram__bytes_write.sum,lts__t_sector_hit_rate.pct,branch uniformity --clock-control none; "
                   "the timed step of `bench.py --ks K --steps 1 --warmup 3`)")
     json.dump({"cfg4": s}, open("profiles/ncu_summary.json", "w"), indent=1)
