@@ -1777,12 +1777,14 @@ __device__ __forceinline__ void run_rounds_tab(const T2Args &a, const ThrWin &w,
                 fin = false;
             }
             const uint32_t tm = tau & ~lmask;
+            // table words of this walk: first slot (13 bits) | length (9) | window row (6)
             int n = 0;
             {
                 const int nrows = fin ? 2 * layers + 1 : 0;
                 const int rmax = __reduce_max_sync(GHN_FULL, nrows);
                 const float r2f = (float)thr_upper(tm, lmask) * 1.0001f;
                 int jw = 0;
+                bool toolong = false;
                 for (int j = 0; j < rmax; ++j) {
                     const int ra = j - layers;
                     int ca = -layers, cb = layers;
@@ -1791,38 +1793,53 @@ __device__ __forceinline__ void run_rounds_tab(const T2Args &a, const ThrWin &w,
                     if (rowon) thr_rect_slots(w, lr, lc, ra, ca, cb, s0, e0);
                     if (e0 > s0) {
                         GHN_ASSERT(jw < nrw - 1);
-                        myr[jw * TT_THREADS] = (uint32_t)s0 | ((uint32_t)e0 << 16);
+                        toolong |= e0 - s0 > 511;
+                        myr[jw * TT_THREADS] = (uint32_t)s0 | ((uint32_t)(e0 - s0) << 13) | ((uint32_t)(lr + ra) << 22);
                         ++jw;
                         n += e0 - s0;
                     }
                 }
-                myr[jw * TT_THREADS] = SB_SENT;
+                myr[jw * TT_THREADS] = 511u << 13;   // closes the table: slots [0, 511), row 0
+                if (fin && toolong) {   // (a row of more than 511 candidates inside the k-th radius)
+                    push_fallback(a, qi);
+                    fin = false;
+                    n = 0;
+                }
             }
             const int steps = __reduce_max_sync(GHN_FULL, n);
-            SelWalk wk;
-            wk.start(myr_s, fin);
+            uint32_t tp = myr_s;
+            uint32_t wd = fin ? lds_u32(tp) : (511u << 13);
+            int p = (int)(wd & 0x1fffu), e = p + (int)((wd >> 13) & 0x1ffu), dlt = w.delta[wd >> 22];
+            tp += TT_THREADS * 4;
+            uint32_t nxw = lds_u32(tp);
             int m = 0;   // members written
             for (int it = 0; it < steps; ++it) {
-                const int p = wk.p;
+                GHN_ASSERT(p >= 0 && p <= a.cap);
                 const float2 c = lds_f2(xy_s + 8u * (uint32_t)p);
                 const uint32_t pk = thr_pack(c, q0, q1, 0u, lmask);
                 const bool mem = it < n && pk <= tm;
                 if (__any_sync(GHN_FULL, mem)) {
                     if (mem && m < k) {
-                        int lo = 0, hi = w.R - 1;   // the window row holding slot p
-                        while (lo < hi) {
-                            const int mid = (lo + hi + 1) >> 1;
-                            if (w.rstart[mid] <= p) lo = mid;
-                            else hi = mid - 1;
-                        }
                         // (the CSR slot; nb_sort_kernel turns it into the point index: a
                         // dependent global load here would stall the lock-step walk)
                         a.out_dist[(int64_t)qi * k + m] = thr_key(c, q0, q1);
-                        a.out_idx[(int64_t)qi * k + m] = (int64_t)(p + w.delta[lo]);
+                        a.out_idx[(int64_t)qi * k + m] = (int64_t)(p + dlt);
                     }
                     m += mem ? 1 : 0;
                 }
-                wk.step();
+                // the walk (SelWalk with this table's word format); a lane past its
+                // rows idles over the closing word's slots
+                p = min(p + 1, a.cap);
+                const bool adv = p >= e;
+                if (__any_sync(GHN_FULL, adv)) {
+                    const uint32_t wn = adv ? nxw : wd;
+                    wd = wn;
+                    p = adv ? (int)(wn & 0x1fffu) : p;
+                    e = adv ? p + (int)((wn >> 13) & 0x1ffu) : e;
+                    dlt = adv ? w.delta[wn >> 22] : dlt;
+                    tp += adv ? TT_THREADS * 4 : 0;
+                    nxw = lds_u32(tp);
+                }
             }
             if (fin && m != k) {   // (cannot happen with a clean k-th boundary; the generic kernel decides)
                 push_fallback(a, qi);
