@@ -22,7 +22,7 @@ struct QArgs {
     int32_t mode;
     int32_t task;
     const int32_t *qorder;
-    const int32_t *nq_dev;   // device count (fallback list); overrides nq when set
+    const int32_t *nq_dev;   // device count (fallback list); overrides nq when set; nq_dev[1] = work cursor (zeroed)
     ghn_query_out out;
 };
 

@@ -851,6 +851,20 @@ __device__ __forceinline__ void query_one(const QArgs &a, int64_t w) {
 template <typename T, int D, int KS, bool SUB>
 __global__ void __launch_bounds__(Q_THREADS, KS <= 2 ? 4 : (KS == 4 ? 3 : 2)) query_kernel(const QArgs a) {
     const int64_t nqv = a.nq_dev ? (int64_t)*a.nq_dev : a.nq;
+    if (a.nq_dev) {
+        // the tiled path's fallback list: a few thousand queries of very
+        // different cost -- warps draw them from a cursor (nq_dev[1], zeroed
+        // with the count) instead of striding
+        int32_t *cursor = const_cast<int32_t *>(a.nq_dev) + 1;
+        for (;;) {
+            int32_t w = 0;
+            if ((threadIdx.x & 31) == 0) w = atomicAdd(cursor, 1);
+            w = __shfl_sync(GHN_FULL, w, 0);
+            if (w >= nqv) break;
+            query_one<T, D, KS, SUB>(a, w);
+        }
+        return;
+    }
     for (int64_t w = (int64_t)blockIdx.x * Q_WARPS + (threadIdx.x >> 5); w < nqv;
          w += (int64_t)gridDim.x * Q_WARPS)
         query_one<T, D, KS, SUB>(a, w);
@@ -859,7 +873,7 @@ __global__ void __launch_bounds__(Q_THREADS, KS <= 2 ? 4 : (KS == 4 ? 3 : 2)) qu
 // ------------------------------------------------------------ launch
 template <typename T, int D, bool SUB>
 int32_t launch_query_d(const QArgs &a, int ks, cudaStream_t s) {
-    int64_t g = a.nq_dev ? (int64_t)sm_count() * 8 : (a.nq + Q_WARPS - 1) / Q_WARPS;
+    int64_t g = a.nq_dev ? (int64_t)sm_count() * 4 : (a.nq + Q_WARPS - 1) / Q_WARPS;
     if (g > 0x7fffffffLL) g = 0x7fffffffLL;
     const unsigned grid = (unsigned)g;
     switch (ks) {

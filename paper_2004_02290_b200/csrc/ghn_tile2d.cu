@@ -1279,7 +1279,7 @@ int32_t tile2d_run(const ghn_index_view *ix, const Tile2dPlan *plan, const void 
     int32_t *fbc = (int32_t *)(ws + 3 * q4 + 2 * t4);
     char *sws = ws + 3 * q4 + 3 * t4;
     GHN_CUDA_CHECK(cudaMemsetAsync(tstart, 0, (size_t)(plan->ntiles + 1) * 4, s));
-    GHN_CUDA_CHECK(cudaMemsetAsync(fbc, 0, 4, s));
+    GHN_CUDA_CHECK(cudaMemsetAsync(fbc, 0, 8, s));   // the fallback count and the generic kernel's cursor over the list
     unsigned g = (unsigned)((nq + 255) / 256);
     if (g > (unsigned)sm_count() * 16) g = (unsigned)sm_count() * 16;
     tile_key_kernel<<<g, 256, 0, s>>>(Q, q_dtype, nq, ix->widths[0], ix->widths[1], inv_w[0], inv_w[1],
