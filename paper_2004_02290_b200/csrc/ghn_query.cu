@@ -80,8 +80,9 @@ extern "C" size_t ghn_query_workspace_size(const ghn_index_view *ix, int64_t nq,
         return lk > b ? lk : b;
     }
     Tile2dPlan tp;
-    for (int stats = 0; stats < 2; ++stats)   // the tiling depends on whether QueryStats are requested
-        if (tile2d_plan(ix, nq, k, GHN_TASK_CLASSIFY, false, stats != 0, &tp)) {
+    // the tiling depends on whether QueryStats are requested and on vote / neighbours
+    for (int v = 0; v < 4; ++v)
+        if (tile2d_plan(ix, nq, k, (v & 2) ? GHN_TASK_NONE : GHN_TASK_CLASSIFY, (v & 2) != 0, (v & 1) != 0, &tp)) {
             size_t t = tile2d_workspace_bytes(&tp, nq);
             if (t > b) b = t;
         }

@@ -1,0 +1,7 @@
+// ghn_query_f64_d0s_k1.cu -- generic predict kernel, double index, runtime d, nested grids, 1 top-k entries per lane
+// (one translation unit per instantiation: they compile in parallel).
+#include "ghn_query_impl.cuh"
+
+namespace ghn {
+int32_t launch_query_f64_d0s_k1(const QArgs &a, cudaStream_t s) { return launch_query_one<double, 0, 1, true>(a, s); }
+}  // namespace ghn

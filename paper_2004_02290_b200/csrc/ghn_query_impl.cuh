@@ -871,6 +871,17 @@ __global__ void __launch_bounds__(Q_THREADS, KS <= 2 ? 4 : (KS == 4 ? 3 : 2)) qu
 }
 
 // ------------------------------------------------------------ launch
+// One (T, D, KS, SUB) instantiation (the nested-grid runtime-d kernels compile
+// for minutes each: one translation unit per KS).
+template <typename T, int D, int KS, bool SUB>
+int32_t launch_query_one(const QArgs &a, cudaStream_t s) {
+    int64_t g = a.nq_dev ? (int64_t)sm_count() * 4 : (a.nq + Q_WARPS - 1) / Q_WARPS;
+    if (g > 0x7fffffffLL) g = 0x7fffffffLL;
+    query_kernel<T, D, KS, SUB><<<(unsigned)g, Q_THREADS, 0, s>>>(a);
+    GHN_LAUNCH_CHECK("query_kernel");
+    return GHN_OK;
+}
+
 template <typename T, int D, bool SUB>
 int32_t launch_query_d(const QArgs &a, int ks, cudaStream_t s) {
     int64_t g = a.nq_dev ? (int64_t)sm_count() * 4 : (a.nq + Q_WARPS - 1) / Q_WARPS;
@@ -887,28 +898,6 @@ int32_t launch_query_d(const QArgs &a, int ks, cudaStream_t s) {
     }
     GHN_LAUNCH_CHECK("query_kernel");
     return GHN_OK;
-}
-
-// Kernels are specialised for the dimensions the configs use (2, 3, 4, 6) on
-// fp32 indexes; everything else (fp64 indexes, other d) runs the runtime-d
-// instantiation -- same arithmetic, loops not unrolled.  Indexes with nested
-// grids run the SUB instantiation (d = 4 specialised: cfg3).
-template <typename T>
-int32_t launch_query(const QArgs &a, int ks, cudaStream_t s) {
-    if (a.ix.n_sub > 0) {
-        if (sizeof(T) == 4 && a.ix.d == 4) return launch_query_d<T, 4, true>(a, ks, s);
-        return launch_query_d<T, 0, true>(a, ks, s);
-    }
-    if (sizeof(T) == 4) {
-        switch (a.ix.d) {
-            case 2: return launch_query_d<T, 2, false>(a, ks, s);
-            case 3: return launch_query_d<T, 3, false>(a, ks, s);
-            case 4: return launch_query_d<T, 4, false>(a, ks, s);
-            case 6: return launch_query_d<T, 6, false>(a, ks, s);
-            default: break;
-        }
-    }
-    return launch_query_d<T, 0, false>(a, ks, s);
 }
 
 }  // namespace

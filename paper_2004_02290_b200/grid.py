@@ -72,12 +72,17 @@ class _Labels:
             if t.dtype.is_floating_point:
                 self._targets = t.to(torch.float64).contiguous()
             else:
-                lo, hi = (torch.aminmax(t) if t.numel() else (torch.zeros(()), torch.zeros(())))
-                lo, hi = int(lo), int(hi)
-                if lo < -2**31 or hi >= 2**31:
-                    raise ValueError("integer labels must fit in int32")
+                wide = t.dtype not in (torch.int32, torch.int16, torch.int8, torch.uint8, torch.bool)
+                if wide and t.numel():
+                    # only a wider dtype needs the range check before the int32 cast; the
+                    # code range itself (n_codes: which vote kernel a predict may use) is
+                    # found on first use, not by the fit -- the reference's build never
+                    # looks at the labels either (grid.py:165-195)
+                    lo, hi = (int(v) for v in torch.aminmax(t))
+                    if lo < -2**31 or hi >= 2**31:
+                        raise ValueError("integer labels must fit in int32")
+                    self._n_codes = hi + 1 if lo >= 0 else 0
                 self.codes = t if t.dtype == torch.int32 and t.is_contiguous() else t.to(torch.int32).contiguous()
-                self._n_codes = hi + 1 if lo >= 0 and t.numel() else 0
                 self._targets_from_codes = True
             return
         try:
@@ -377,16 +382,17 @@ def build_arrays(X, y=None, params: GridParams | None = None, cells_per_axis=Non
     s = _lib.stream_handle()
     widths = np.ascontiguousarray(params.widths, dtype=np.float64)
     wptr = widths.ctypes.data_as(ctypes.c_void_p)
-    bounds = torch.empty(2 * d, dtype=torch.int64, device=dev)
-    origin = torch.empty(d, dtype=torch.float64, device=dev)
-    flags = torch.zeros(1, dtype=torch.int32, device=dev)
+    # bounds (2d int64), origin (d fp64) and the non-finite flag in one buffer: one read-back
+    kbuf = torch.zeros(3 * d + 1, dtype=torch.int64, device=dev)
+    bounds, origin, flags = kbuf[:2 * d], kbuf[2 * d:3 * d].view(torch.float64), kbuf[3 * d:].view(torch.int32)
     _lib.check(L.ghn_fit_bounds(_lib.ptr(Xd), dtype, n, d, wptr, _lib.ptr(bounds), _lib.ptr(origin),
                                 _lib.ptr(flags), s), "ghn_fit_bounds")
-    if int(flags.item()) & 1:
+    kh = kbuf.cpu()
+    if int(kh[3 * d:].view(torch.int32)[0]) & 1:
         raise ValueError("non-finite coordinate")
-    bh = np.ascontiguousarray(bounds.cpu().numpy())
+    bh = np.ascontiguousarray(kh[:2 * d].numpy())
     if C is not None:
-        params = GridParams(params.widths, origin.cpu().numpy(), params.splits)
+        params = GridParams(params.widths, kh[2 * d:3 * d].view(torch.float64).numpy().copy(), params.splits)
     plan = _lib.FitPlan()
     _lib.check(L.ghn_fit_plan_init(ctypes.byref(plan), n, d, dtype, wptr,
                                    bh.ctypes.data_as(ctypes.c_void_p), dense_limit_for(n)),

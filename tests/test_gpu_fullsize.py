@@ -58,6 +58,36 @@ def test_cfg4_full(ghn, k, cfg4_full):
     _sample_check(ghn, index, ref, w, w.Q, k, "classify", rng)
 
 
+@pytest.mark.parametrize("k", [1, 4, 16, 64])
+def test_cfg4_full_no_stats(ghn, k, cfg4_full):
+    """The benchmarked instantiation at the benchmarked plan: no QueryStats
+    (its own tile side and apron), labels + confidences on a 20,000-query sample."""
+    import torch
+
+    index, ref, w = cfg4_full
+    rng = np.random.default_rng(4100 + k)
+    r = ghn.predict_batch(index, torch.from_numpy(w.Q).cuda(), k, "heuristic")
+    sel = np.sort(rng.choice(w.Q.shape[0], size=20000, replace=False))
+    keys, idx, _ = ref.query(w.Q[sel], k, "heuristic")
+    lab, conf = oracle.classify(keys, idx, np.asarray(w.y, dtype=np.int64))
+    assert np.array_equal(r["label"].cpu().numpy()[sel].astype(np.int64), lab)
+    assert np.array_equal(r["confidence"].cpu().numpy()[sel], conf)
+
+
+def test_cfg4_full_neighbors(ghn, cfg4_full):
+    """knn_query_batch at the full size (tile2d_nb_kernel): indices and distances."""
+    import torch
+
+    index, ref, w = cfg4_full
+    rng = np.random.default_rng(4200)
+    dist, idx, _ = ghn.knn_query_batch(index, torch.from_numpy(w.Q).cuda(), 16, stats=False)
+    sel = np.sort(rng.choice(w.Q.shape[0], size=10000, replace=False))
+    keys, ridx, _ = ref.query(w.Q[sel], 16, "heuristic")
+    sd = torch.from_numpy(sel).cuda()
+    assert np.array_equal(idx[sd].cpu().numpy(), ridx)
+    assert np.array_equal(dist[sd].cpu().numpy(), np.sqrt(keys))
+
+
 @pytest.fixture(scope="module")
 def cfg4_full(ghn):
     from paper_2004_02290_b200 import datagen
