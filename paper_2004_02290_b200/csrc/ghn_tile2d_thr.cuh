@@ -1528,6 +1528,8 @@ __device__ __forceinline__ uint32_t tab_pack(uint32_t xy_s, uint32_t sl_s, int p
     return thr_pack(lds_f2(xy_s + 8u * (uint32_t)p), q0, q1, lds_u8(sl_s + (uint32_t)p), lmask);
 }
 
+constexpr uint32_t NB_CLOSE = 511u << 13;   // closing word of the neighbour walk's table (slots [0, 511), row 0)
+
 template <int KM, bool STATS, bool NB>
 __device__ __forceinline__ void run_rounds_tab(const T2Args &a, const ThrWin &w, uint32_t *rtab, int nrw,
                                                const uint16_t *ord, const uint32_t *info, int *s_grp, int qb, int qe,
@@ -1777,29 +1779,32 @@ __device__ __forceinline__ void run_rounds_tab(const T2Args &a, const ThrWin &w,
                 fin = false;
             }
             const uint32_t tm = tau & ~lmask;
-            // table words of this walk: first slot (13 bits) | length (9) | window row (6)
+            // The members lie in the layers whose data was read: a last layer beyond
+            // the apron was only visited because it provably holds none.
+            const int le = min(layers, a.A);
+            // table words of this walk: first slot (13 bits) | length (9) | window row (7)
             int n = 0;
             {
-                const int nrows = fin ? 2 * layers + 1 : 0;
+                const int nrows = fin ? 2 * le + 1 : 0;
                 const int rmax = __reduce_max_sync(GHN_FULL, nrows);
                 const float r2f = (float)thr_upper(tm, lmask) * 1.0001f;
                 int jw = 0;
                 bool toolong = false;
                 for (int j = 0; j < rmax; ++j) {
-                    const int ra = j - layers;
-                    int ca = -layers, cb = layers;
-                    const bool rowon = clip.cols(ra, layers, r2f, ca, cb) && j < nrows;
+                    const int ra = j - le;
+                    int ca = -le, cb = le;
+                    const bool rowon = clip.cols(ra, le, r2f, ca, cb) && j < nrows;
                     int s0 = 0, e0 = 0;
                     if (rowon) thr_rect_slots(w, lr, lc, ra, ca, cb, s0, e0);
                     if (e0 > s0) {
-                        GHN_ASSERT(jw < nrw - 1);
+                        GHN_ASSERT(jw < nrw - 1 && lr + ra >= 0 && lr + ra < 128);
                         toolong |= e0 - s0 > 511;
                         myr[jw * TT_THREADS] = (uint32_t)s0 | ((uint32_t)(e0 - s0) << 13) | ((uint32_t)(lr + ra) << 22);
                         ++jw;
                         n += e0 - s0;
                     }
                 }
-                myr[jw * TT_THREADS] = 511u << 13;   // closes the table: slots [0, 511), row 0
+                myr[jw * TT_THREADS] = NB_CLOSE;   // closes the table: slots [0, 511) of row 0, entered again and again
                 if (fin && toolong) {   // (a row of more than 511 candidates inside the k-th radius)
                     push_fallback(a, qi);
                     fin = false;
@@ -1808,9 +1813,9 @@ __device__ __forceinline__ void run_rounds_tab(const T2Args &a, const ThrWin &w,
             }
             const int steps = __reduce_max_sync(GHN_FULL, n);
             uint32_t tp = myr_s;
-            uint32_t wd = fin ? lds_u32(tp) : (511u << 13);
+            uint32_t wd = fin ? lds_u32(tp) : NB_CLOSE;
             int p = (int)(wd & 0x1fffu), e = p + (int)((wd >> 13) & 0x1ffu), dlt = w.delta[wd >> 22];
-            tp += TT_THREADS * 4;
+            tp += wd != NB_CLOSE ? TT_THREADS * 4 : 0;   // (the prefetch never passes the closing word)
             uint32_t nxw = lds_u32(tp);
             int m = 0;   // members written
             for (int it = 0; it < steps; ++it) {
@@ -1837,7 +1842,7 @@ __device__ __forceinline__ void run_rounds_tab(const T2Args &a, const ThrWin &w,
                     p = adv ? (int)(wn & 0x1fffu) : p;
                     e = adv ? p + (int)((wn >> 13) & 0x1ffu) : e;
                     dlt = adv ? w.delta[wn >> 22] : dlt;
-                    tp += adv ? TT_THREADS * 4 : 0;
+                    tp += adv && wn != NB_CLOSE ? TT_THREADS * 4 : 0;
                     nxw = lds_u32(tp);
                 }
             }

@@ -69,3 +69,29 @@ def test_neighbors_duplicates_and_outliers(ghn):
                         (rng.random((200, 2), dtype=np.float32) * 3 - 1).astype(np.float32)])
     for k in (3, 16):
         _check(ghn, index, ref, Q, k, "heuristic", True)
+
+
+def test_clustered_dense_rows(ghn):
+    """Clustered data: dense cells (long clipped rows, tiles of very different
+    work), queries from the same mixture.  Neighbours and the fused vote."""
+    rng = np.random.default_rng(74)
+    n, nq, C = 3_000_000, 300_000, 512
+    means = rng.random((12, 2))
+    comp = rng.integers(0, 12, n)
+    X = np.clip(means[comp] + rng.normal(0, 0.02, (n, 2)), 0, 1).astype(np.float32)
+    y = (comp % 4).astype(np.int32)
+    Q = np.clip(means[rng.integers(0, 12, nq)] + rng.normal(0, 0.02, (nq, 2)), 0, 1).astype(np.float32)
+    index = ghn.build_arrays(X, y, cells_per_axis=C)
+    ref = oracle.COracle(X, np.full(2, 1.0 / C))
+    sel = np.sort(rng.choice(nq, size=3000, replace=False))
+    for k in (1, 16, 32):
+        dist, idx, _ = ghn.knn_query_batch(index, Q, k, stats=False)
+        keys, ridx, _ = ref.query(Q[sel], k, "heuristic")
+        assert np.array_equal(idx.cpu().numpy()[sel], ridx), f"k={k}: indices"
+        assert np.array_equal(dist.cpu().numpy()[sel], np.sqrt(keys)), f"k={k}: distances"
+    for k in (4, 64):
+        p = ghn.predict_batch(index, Q, k)
+        keys, ridx, _ = ref.query(Q[sel], k, "heuristic")
+        lab, conf = oracle.classify(keys, ridx, y.astype(np.int64))
+        assert np.array_equal(p["label"].cpu().numpy()[sel].astype(np.int64), lab), f"k={k}: labels"
+        assert np.array_equal(p["confidence"].cpu().numpy()[sel], conf), f"k={k}: confidences"
