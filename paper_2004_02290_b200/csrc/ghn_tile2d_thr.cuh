@@ -967,7 +967,7 @@ __device__ __forceinline__ void sel_pass2(uint32_t xy_s, uint32_t sl_s, uint32_t
             const uint32_t inc = __funnelshift_l(0u, 1u, lab8);   // 1 << lab8, lab8 <= 24
             cn += vote ? (cnt_t)inc : (cnt_t)0;
         }
-        GHN_ASSERT(wk.p >= 0 && wk.p < 65536 && np < note_s + (uint32_t)SB_NOTE * TT_THREADS * 4);
+        GHN_ASSERT(wk.p >= 0 && wk.p < 65536 && (!note || np < note_s + (uint32_t)SB_NOTE * TT_THREADS * 4));
         if (note) asm volatile("st.shared.u16 [%0], %1;" ::"r"(np), "h"((uint16_t)wk.p) : "memory");
         np += note ? TT_THREADS * 4 : 0;
         // (SKIP: the histogram does not bound the boundary members; past the

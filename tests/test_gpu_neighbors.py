@@ -89,6 +89,14 @@ def test_clustered_dense_rows(ghn):
         keys, ridx, _ = ref.query(Q[sel], k, "heuristic")
         assert np.array_equal(idx.cpu().numpy()[sel], ridx), f"k={k}: indices"
         assert np.array_equal(dist.cpu().numpy()[sel], np.sqrt(keys)), f"k={k}: distances"
+    # few queries: the largest tiles (windows of up to 72 rows)
+    few = 20000
+    for k in (1, 16):
+        dist, idx, st = ghn.knn_query_batch(index, Q[:few], k, stats=True)
+        keys, ridx, rst = ref.query(Q[:few], k, "heuristic")
+        assert np.array_equal(idx.cpu().numpy(), ridx), f"k={k}: indices (few queries)"
+        assert np.array_equal(dist.cpu().numpy(), np.sqrt(keys)), f"k={k}: distances (few queries)"
+        assert np.array_equal(st.cpu().numpy(), rst), f"k={k}: QueryStats (few queries)"
     for k in (4, 64):
         p = ghn.predict_batch(index, Q, k)
         keys, ridx, _ = ref.query(Q[sel], k, "heuristic")
