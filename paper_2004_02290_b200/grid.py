@@ -132,7 +132,9 @@ class _Labels:
         if not hasattr(self, "_n_codes"):
             self._n_codes = 0
             if self.codes is not None and self.codes.numel():
-                lo, hi = int(self.codes.min()), int(self.codes.max())
+                import torch
+
+                lo, hi = (int(v) for v in torch.aminmax(self.codes))   # one pass, one read-back
                 self._n_codes = hi + 1 if lo >= 0 and hi < 2**31 - 1 else 0
         return self._n_codes
 
@@ -236,10 +238,12 @@ class GridIndex:
         return self._cache["table"]
 
     # -- device view ----------------------------------------------------------
-    def view(self, density: bool = True, targets: bool = True) -> _lib.IndexView:
+    def view(self, density: bool = True, targets: bool = True, label_range: bool = True) -> _lib.IndexView:
         """ctypes ghn_index_view of the device tables (density=False skips
         the tiled predict's density hint, which costs a kernel + sync once;
-        targets=False leaves the fp64 regression targets unmaterialised)."""
+        targets=False leaves the fp64 regression targets unmaterialised;
+        label_range=False leaves the label code range -- one reduction over
+        the labels on first use -- to the first predict)."""
         v = _lib.IndexView()
         p = self.plan
         v.n, v.d, v.dtype, v.layout, v.n_cells, v.E = p.n, p.d, p.dtype, p.layout, self.n_cells, p.E
@@ -257,7 +261,7 @@ class GridIndex:
         v.labels = _lib.ptr(self._labels.codes)
         v.targets = _lib.ptr(self._labels.targets) if targets else 0
         v.labels_perm = _lib.ptr(self.labels_perm)
-        v.n_labels = self._labels.n_codes
+        v.n_labels = self._labels.n_codes if label_range else 0
         v.metric = _lib.GHN_METRIC[self.metric]
         v.density_hint = self.density_hint(v) if density else 0.0
         sg = self._subgrids
@@ -461,7 +465,7 @@ def _build_subgrids(index: GridIndex, min_points: int = SUBGRID_MIN_POINTS) -> N
         return
     dev = index.X.device
     s = _lib.stream_handle()
-    v = index.view(density=False, targets=False)
+    v = index.view(density=False, targets=False, label_range=False)
     cap = n // (min_points + 1) + 1
     cells = torch.empty(cap, dtype=torch.int32, device=dev)
     cnt = torch.zeros(1, dtype=torch.int32, device=dev)
