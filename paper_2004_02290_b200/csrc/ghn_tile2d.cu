@@ -1149,6 +1149,10 @@ bool tile2d_plan(const ghn_index_view *ix, int64_t nq, int32_t k, int32_t task, 
     if (ix->density_hint > rho) rho = ix->density_hint;
     int lf = 0;
     while (lf < 8 && (2.0 * lf + 1) * (2.0 * lf + 1) * rho < (double)k) ++lf;
+    // sparse for this k: the typical query needs layers beyond any apron a tile
+    // can stage (4), so nearly every query would end on the fallback list after
+    // the staging was paid (0.5 points per cell at k = 64: lf = 6)
+    if (lf + 1 > 4) return false;
     // apron: two layers beyond the layer that fills the buffer on average.  The
     // thread kernels without QueryStats need one: a shell beyond the apron that
     // provably cannot change the top-k is skipped without its data.
