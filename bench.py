@@ -672,7 +672,7 @@ def run_ours(args):
             kc = list(wc.ks) or [wc.k]
             mc = measure(wc, kc, flush, stream, args.config_steps, 3)
             refc = oracle.COracle(wc.X, wc.widths)
-            samp = {0: 10000, 3: 1000}.get(c, args.parity_sample)
+            samp = {0: 10000, 3: 300}.get(c, args.parity_sample)
             par = [parity_check(wc, k, mc["outs"][k], refc, samp, 8000 + c) for k in kc]
             del refc
             configs[f"cfg{c}"] = config_block(c, wc, mc, peak, peak_kind, fpp, par)

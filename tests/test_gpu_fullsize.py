@@ -128,13 +128,14 @@ def test_cfg1_cfg2_full(ghn, cfg):
 
 
 def test_cfg3_full_training_set_sampled_queries(ghn):
-    """cfg3: 50M lognormal points, one cell holding ~36M of them; 300 seeded
-    queries (90 % data-distributed, 10 % uniform) through the generic kernel."""
+    """cfg3: 50M lognormal points, one cell holding ~36M of them; 1,000 seeded
+    queries (90 % data-distributed, 10 % uniform) through the generic kernel
+    (nested grids + lower-bound pruning)."""
     from paper_2004_02290_b200 import datagen
 
-    w = datagen.cfg3(nq=300)
+    w = datagen.cfg3(nq=1000)
     index = ghn.build_arrays(w.X, w.y, cells_per_axis=w.cells_per_axis)
     ref = oracle.COracle(w.X, w.widths)
     _fit_check(index, ref)
     assert np.diff(index.bucket_starts).max() > 30_000_000     # the fat cell
-    _sample_check(ghn, index, ref, w, w.Q, w.k, "classify", np.random.default_rng(3), nsample=300)
+    _sample_check(ghn, index, ref, w, w.Q, w.k, "classify", np.random.default_rng(3), nsample=1000)
