@@ -340,6 +340,15 @@ __device__ __forceinline__ uint32_t point_key(const T *__restrict__ X, int64_t i
     return (uint32_t)key;
 }
 
+// These histograms serve the sets the streaming fit leaves (a key range too
+// heavy for a CTA: cfg3 puts 36M of its 50M points in one cell), so lanes of
+// a warp often share a cell: one atomic per distinct key and warp
+// (__match_any_sync), not 32 serialised ones on the same counter.
+__device__ __forceinline__ void hist_add_agg(uint32_t *ctr, uint32_t key, uint32_t slot, uint32_t unit) {
+    const unsigned peers = __match_any_sync(__activemask(), key);
+    if ((int)(threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(ctr + slot, unit * (uint32_t)__popc(peers));
+}
+
 template <typename T>
 __global__ void __launch_bounds__(FIT_THREADS) hist_kernel(const T *__restrict__ X, int64_t n, DimParams p,
                                                            int32_t *__restrict__ counts) {
@@ -351,7 +360,7 @@ __global__ void __launch_bounds__(FIT_THREADS) hist_kernel(const T *__restrict__
 #pragma unroll
         for (int u = 0; u < BU; ++u) key[u] = point_key(X, i + u * stride, p);
 #pragma unroll
-        for (int u = 0; u < BU; ++u) atomicAdd(&counts[key[u]], 1);
+        for (int u = 0; u < BU; ++u) hist_add_agg((uint32_t *)counts, key[u], key[u], 1u);
     }
     for (; i < n; i += stride) atomicAdd(&counts[point_key(X, i, p)], 1);
 }
@@ -373,7 +382,7 @@ __global__ void __launch_bounds__(FIT_THREADS) hist16_kernel(const T *__restrict
 #pragma unroll
         for (int u = 0; u < BU; ++u) key[u] = point_key(X, i + u * stride, p);
 #pragma unroll
-        for (int u = 0; u < BU; ++u) atomicAdd(&packed[key[u] >> 1], 1u << (16 * (key[u] & 1u)));
+        for (int u = 0; u < BU; ++u) hist_add_agg(packed, key[u], key[u] >> 1, 1u << (16 * (key[u] & 1u)));
     }
     for (; i < n; i += stride) {
         const uint32_t key = point_key(X, i, p);
