@@ -54,6 +54,9 @@ namespace {
 #endif
 
 constexpr int TT_THREADS = 256;
+#ifndef GHN_TT_NOSORT_KM
+#define GHN_TT_NOSORT_KM 2   // list capacities up to this keep the tile's query order (no counting sort by work)
+#endif
 #ifndef GHN_TT_TAB
 #define GHN_TT_TAB 1   // k <= 32: table-driven rounds (run_rounds_tab); 0: the round-1 rounds, for A/B builds
 #endif
@@ -472,7 +475,15 @@ __device__ __forceinline__ uint32_t sel_prep(const T2Args &a, const ThrWin &w, i
 // sorted by (skip-ahead, candidate count 0..255, larger clamped): a counting sort.
 __device__ __forceinline__ void sel_sort_chunk(const T2Args &a, const ThrWin &w, int c0, int c1, int t0, int t1,
                                                int r_lo, int c_lo, int *hcnt, uint16_t *kr, uint16_t *ord,
-                                               uint32_t *info, bool allow_skip) {
+                                               uint32_t *info, bool allow_skip, bool order = true) {
+    if (!order) {   // phase A only, queries in tile order (k <= GHN_TT_NOSORT_K: the sort costs more than it saves)
+        for (int i = threadIdx.x; i < c1 - c0; i += TT_THREADS) {
+            info[i] = sel_prep(a, w, a.qorder[c0 + i], t0, t1, r_lo, c_lo, allow_skip);
+            ord[i] = (uint16_t)i;
+        }
+        __syncthreads();
+        return;
+    }
     for (int i = threadIdx.x; i < 512; i += TT_THREADS) hcnt[i] = 0;
     __syncthreads();
     for (int i = threadIdx.x; i < c1 - c0; i += TT_THREADS) {
@@ -1961,7 +1972,8 @@ __device__ __forceinline__ void tile2d_thr_body(const T2Args &a) {
         for (int c0 = qb; c0 < qe; c0 += SB_SORT_N) {
             const int c1 = min(c0 + SB_SORT_N, qe);
             if (threadIdx.x == 0) s_grp = 0;
-            sel_sort_chunk(a, w, c0, c1, t0, t1, r_lo, c_lo, (int *)rtab, (uint16_t *)(rtab + 512), s_ord, s_info, false);
+            sel_sort_chunk(a, w, c0, c1, t0, t1, r_lo, c_lo, (int *)rtab, (uint16_t *)(rtab + 512), s_ord, s_info, false,
+                           KM > GHN_TT_NOSORT_KM);
             run_rounds_tab<KM == 0 ? 1 : KM, STATS, NB>(a, w, rtab, nrw, s_ord, s_info, &s_grp, c0, c1, r_lo, c_lo, tot);
             __syncthreads();
         }
