@@ -244,6 +244,12 @@ class GridIndex:
         targets=False leaves the fp64 regression targets unmaterialised;
         label_range=False leaves the label code range -- one reduction over
         the labels on first use -- to the first predict)."""
+        # (built once per flag combination: the tables never move; the nested
+        # grids, attached once after the fit, drop the cached views)
+        vkey = (density, targets, label_range)
+        cached = self._cache.get("views", {}).get(vkey)
+        if cached is not None:
+            return cached
         v = _lib.IndexView()
         p = self.plan
         v.n, v.d, v.dtype, v.layout, v.n_cells, v.E = p.n, p.d, p.dtype, p.layout, self.n_cells, p.E
@@ -270,6 +276,7 @@ class GridIndex:
             v.sub_of_cell, v.subs = _lib.ptr(sg["sub_of_cell"]), _lib.ptr(sg["subs"])
             v.sub_off, v.sub_coords, v.sub_idx = _lib.ptr(sg["sub_off"]), _lib.ptr(sg["coords"]), _lib.ptr(sg["idx"])
             v.n_subpts = sg["n_points"]
+        self._cache.setdefault("views", {})[vkey] = v
         return v
 
     @property
@@ -510,6 +517,7 @@ def _build_subgrids(index: GridIndex, min_points: int = SUBGRID_MIN_POINTS) -> N
     _lib.check(L.ghn_subgrid_build(ctypes.byref(v), _lib.ptr(subs), n_sub, e_tot, _lib.ptr(sub_off),
                                    _lib.ptr(coords), _lib.ptr(idx), n_points, _lib.ptr(sub_of_cell),
                                    _lib.ptr(ws), wsz, s), "ghn_subgrid_build")
+    index._cache.pop("views", None)
     index._subgrids = {"n_sub": n_sub, "min_points": min_points, "sub_of_cell": sub_of_cell, "subs": subs,
                        "sub_off": sub_off, "coords": coords, "idx": idx, "n_points": n_points,
                        "records": recs}
