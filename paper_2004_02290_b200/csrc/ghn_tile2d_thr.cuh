@@ -1520,6 +1520,13 @@ struct SelClip {
         mg0 = 1e-4f * w0f;
         mg1 = 1e-4f * w1f;
     }
+    // No point of shell(l) can precede a k-th key whose d-part interval ends at
+    // `upper`: the nearest face of block(l - 1) lies beyond it.  fp32 with the
+    // margins on the safe side (a false "not beyond" only costs the walk).
+    __device__ __forceinline__ bool shell_beyond(int l, double upper) const {
+        const float d = fminf(fminf(fl0, fh0) + (float)(l - 1) * w0f - mg0, fminf(fl1, fh1) + (float)(l - 1) * w1f - mg1);
+        return d > 0.0f && d * d * (1.0f - 1e-4f) > (float)upper * 1.0001f;
+    }
     // Columns [ca, cb] (offsets from q's cell, within -+ls) of row offset ra
     // that can hold a point within sqrt(r2f) of q; false: none.  fp32 with
     // margins far above its rounding (r2f is passed inflated): a superset.
@@ -1677,7 +1684,6 @@ __device__ __forceinline__ void run_rounds_tab(const T2Args &a, const ThrWin &w,
         bool more = live && l < lmax;   // continues with layer l + 1
         bool fin = live && !more;       // answered after layer l
         // ---- C (tab): later layers
-        const RectBound rb0 = more ? RectBound(a, q0, q1, cc0, cc1) : RectBound();
         while (__any_sync(GHN_FULL, more)) {
             uint32_t tm = 0;
             double upper = 0.0;
@@ -1688,7 +1694,7 @@ __device__ __forceinline__ void run_rounds_tab(const T2Args &a, const ThrWin &w,
                 upper = thr_upper(tm, lmask);
                 // the whole shell first (one test, no data): beyond the k-th it
                 // cannot change the top-k, wherever the apron ends
-                act = !rb0.shell_beyond(a, l, upper);
+                act = !clip.shell_beyond(l, upper);
                 if (l > a.A && (STATS || act)) {
                     push_fallback(a, qi);
                     more = false;
